@@ -1,0 +1,137 @@
+/* libdcsvd_b200 — B200-native (sm_100a) fp64 divide-and-conquer SVD.
+ *
+ * C ABI.  Every matrix is float64 column-major with an explicit leading
+ * dimension; every pointer is a DEVICE pointer (e.g. torch `data_ptr()`),
+ * except the option/profile structs which live on the host.  Calls enqueue on
+ * the caller's stream; the handle owns scratch workspace and a device status
+ * word, so use one handle per stream/thread.  Return codes:
+ *   0 ok, 1 invalid argument (ValueError), 2 no convergence
+ *   (ConvergenceError), 3 interlacing violated (ArithmeticError), 4 singular
+ *   triangular factor (LinAlgError), 5 CUDA error (RuntimeError);
+ * dcsvd_last_error() gives the message.
+ *
+ * The reference exposes no FFI: its boundary is the Python module API of the
+ * `dcsvd` package (/root/reference/pkg/src/dcsvd/__init__.py:18-129).  Each
+ * entry point below cites the reference function it replaces; the Python
+ * package paper_2508_11467_b200 keeps those names/signatures and calls these
+ * through ctypes.
+ */
+#ifndef DCSVD_B200_H
+#define DCSVD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dcsvd_ctx* dcsvd_handle;
+
+/* status codes */
+#define DCSVD_OK 0
+#define DCSVD_EINVAL 1
+#define DCSVD_ENOCONV 2
+#define DCSVD_EARITH 3
+#define DCSVD_ESINGULAR 4
+#define DCSVD_ECUDA 5
+
+/* SVDOptions (pkg/src/dcsvd/driver.py:34-63). */
+typedef struct dcsvd_opts {
+  int want_vectors;        /* 1 = U and Vt, 0 = values only              */
+  int bidiag_block;        /* GEBRD panel width (default 32)             */
+  int qr_block;            /* GEQRF panel width (default 32)             */
+  int orgqr_block;         /* ORGQR block width (default 64)             */
+  int apply_block;         /* ORMBR block width (default 64)             */
+  int leaf_size;           /* BDC leaf bound, 1..32 (default 32)         */
+  double ts_crossover;     /* QR-first when m >= ts_crossover*n (5/3)    */
+  double deflation_multiple; /* deflation tolerance multiple (8)         */
+} dcsvd_opts;
+
+/* PhaseProfile (driver.py:76-82): seconds per PHASE_NAMES entry (driver.py:31),
+ * measured with CUDA events on the call's stream. */
+typedef struct dcsvd_phase_times {
+  double geqrf, orgqr, gebrd, bdcdc, ormbr, gemm, total;
+} dcsvd_phase_times;
+
+/* lifecycle ---------------------------------------------------------------- */
+int dcsvd_create(dcsvd_handle* h, int device);
+int dcsvd_destroy(dcsvd_handle h);
+const char* dcsvd_last_error(dcsvd_handle h);
+int dcsvd_version(void);
+/* Number of this library's kernels launched through `h` since creation. */
+long long dcsvd_launch_count(dcsvd_handle h);
+
+/* GEMM: C <- alpha*op(A)*op(B) + beta*C (beta == 0 does not read C).
+ * Replaces densecore.matmul_accumulate (pkg/src/dcsvd/densecore.py:73-93).
+ * Hand-written DMMA (mma.sync m8n8k4 f64) kernel. */
+int dcsvd_dgemm(dcsvd_handle h, int transa, int transb, int64_t m, int64_t n, int64_t k,
+                double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+                double beta, double* C, int64_t ldc, void* stream);
+
+/* GEMV: y <- alpha*op(A)*x + beta*y (densecore.py:96-111). */
+int dcsvd_dgemv(dcsvd_handle h, int transa, int64_t m, int64_t n, double alpha, const double* A,
+                int64_t lda, const double* x, double beta, double* y, void* stream);
+
+/* Blocked bidiagonalization in place, m >= n (bidiag.py:168-204, merged
+ * rank-2b LABRD panel bidiag.py:113-165 + single trailing GEMM).
+ * d[n], e[n-1], tauq[n], taup[n] (taup[n-1] = 0). */
+int dcsvd_gebrd(dcsvd_handle h, int64_t m, int64_t n, double* A, int64_t lda, double* d, double* e,
+                double* tauq, double* taup, int nb, void* stream);
+
+/* One merged rank-2b LABRD panel on the m x n view A (bidiag.py:113-165):
+ * factors the leading nb rows/columns, writes d/e/tauq/taup[0..nb) and the
+ * panel matrices P (m x 2nb, ldp) and Q (n x 2nb, ldq); requires
+ * 1 <= nb < n <= m, nb <= 32.  The trailing update is left to the caller. */
+int dcsvd_labrd(dcsvd_handle h, int64_t m, int64_t n, double* A, int64_t lda, double* d, double* e,
+                double* tauq, double* taup, int nb, double* P, int64_t ldp, double* Q, int64_t ldq,
+                void* stream);
+
+/* Bidiagonal divide and conquer (bdc.py:861-880).  d[n], e[n] (e[n-1] used
+ * only when bordered).  Outputs: dvals[n] descending; edge[2 x ncols]
+ * (ld 2, column-major, i.e. edge[2*j + r]); when want_vectors: W[n x n]
+ * (ldw), Q[ncols x ncols] (ldq), ncols = n + bordered.  W/Q may be NULL when
+ * want_vectors == 0. */
+int dcsvd_bdsdc(dcsvd_handle h, int64_t n, const double* d, const double* e, int bordered,
+                int want_vectors, int leaf, double tol_multiple, double* dvals, double* W,
+                int64_t ldw, double* Q, int64_t ldq, double* edge, void* stream);
+
+/* Blocked Householder QR in place, m >= n (qrblock.py:122-144). */
+int dcsvd_geqrf(dcsvd_handle h, int64_t m, int64_t n, double* A, int64_t lda, double* tau, int nb,
+                void* stream);
+
+/* First k columns of Q from a packed QR of an m x nrefl matrix
+ * (qrblock.py:147-164).  Q is m x k (ldq), overwritten. */
+int dcsvd_orgqr(dcsvd_handle h, int64_t m, int64_t nrefl, int64_t k, const double* A, int64_t lda,
+                const double* tau, double* Q, int64_t ldq, int nb, void* stream);
+
+/* Back-transformation with the bidiagonalization reflectors of the m x n
+ * packed matrix A (backtransform.py:90-131).
+ *   vect = 'Q': C (m x ncols) <- U1 C   (trans = 0)  or U1^T C (trans = 1)
+ *   vect = 'P': C (nrows x n) <- C V1   (trans = 0)  or C V1^T (trans = 1)
+ * tau = tauq (for 'Q') or taup (for 'P'). */
+int dcsvd_ormbr(dcsvd_handle h, char vect, int trans, int64_t m, int64_t n, const double* A,
+                int64_t lda, const double* tau, double* C, int64_t c_rows, int64_t c_cols,
+                int64_t ldc, int nb, void* stream);
+
+/* Economy SVD A = U diag(S) VT of an m x n matrix (driver.py:121-157).
+ * A is consumed as workspace (the Python layer copies first, like the
+ * reference, driver.py:154).  S[min(m,n)] descending; U m x k (ldu), VT k x n
+ * (ldvt) with k = min(m, n); U/VT ignored when opts->want_vectors == 0.
+ * `prof` (optional, host) receives per-phase device seconds. */
+int dcsvd_gesdd(dcsvd_handle h, int64_t m, int64_t n, double* A, int64_t lda, double* S, double* U,
+                int64_t ldu, double* VT, int64_t ldvt, const dcsvd_opts* opts,
+                dcsvd_phase_times* prof, void* stream);
+
+/* Batched independent SVDs of equally sized m x n matrices (BASELINE config
+ * 5).  Arrays of `batch` device pointers (host arrays of device pointers);
+ * leading dimensions shared.  Executes in waves of up to `concurrency`
+ * matrices (0 = automatic). */
+int dcsvd_gesdd_batched(dcsvd_handle h, int batch, int64_t m, int64_t n, double* const* A,
+                        int64_t lda, double* const* S, double* const* U, int64_t ldu,
+                        double* const* VT, int64_t ldvt, const dcsvd_opts* opts, int concurrency,
+                        void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DCSVD_B200_H */

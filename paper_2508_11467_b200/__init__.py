@@ -1,0 +1,78 @@
+"""B200-native fp64 divide-and-conquer SVD (arxiv 2508.11467), drop-in for
+the reference ``dcsvd`` package's SVD path.
+
+Public surface mirrors pkg/src/dcsvd/__init__.py:18-129 for the hot path:
+``gesdd`` (alias ``svd``), ``phase_profile``, ``SVDOptions``, ``SVDResult``,
+``PhaseProfile``, ``PHASE_NAMES``; ``gebrd_blocked`` (alias
+``bidiagonalize``), ``labrd_panel``, ``gebrd_unblocked``,
+``BidiagonalFactorization``, ``PanelWorkspace``; ``bdsdc`` (alias ``bdc``),
+``BidiagonalProblem``, ``SubproblemSVD``; ``geqrf_blocked``, ``orgqr``,
+``QRFactorization``; ``ormqr_like``, ``ormlq_like``, ``ReflectorSequence``,
+``column_reflectors``, ``row_reflectors``; ``matmul_accumulate``,
+``matvec_accumulate``; ``ConvergenceError``; plus ``gesdd_batched``.
+
+Every numeric entry point runs hand-written sm_100a CUDA kernels from
+``libdcsvd_b200.so`` through ctypes.  There is no CPU fallback.
+"""
+
+from ._lib import ConvergenceError, launch_count
+from .bidiagonal import (
+    BidiagonalFactorization,
+    PanelWorkspace,
+    gebrd_blocked,
+    gebrd_unblocked,
+    labrd_panel,
+)
+from .blas import as_dense, dense_matrix, matmul_accumulate, matvec_accumulate
+from .dc import BidiagonalProblem, SubproblemSVD, bdsdc
+from .householder import (
+    QRFactorization,
+    ReflectorSequence,
+    column_reflectors,
+    geqrf_blocked,
+    orgqr,
+    ormlq_like,
+    ormqr_like,
+    row_reflectors,
+)
+from .svd import PHASE_NAMES, PhaseProfile, SVDOptions, SVDResult, gesdd, gesdd_batched, phase_profile, svd
+
+bidiagonalize = gebrd_blocked
+bdc = bdsdc
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BidiagonalFactorization",
+    "BidiagonalProblem",
+    "ConvergenceError",
+    "PHASE_NAMES",
+    "PanelWorkspace",
+    "PhaseProfile",
+    "QRFactorization",
+    "ReflectorSequence",
+    "SVDOptions",
+    "SVDResult",
+    "SubproblemSVD",
+    "as_dense",
+    "bdc",
+    "bdsdc",
+    "bidiagonalize",
+    "column_reflectors",
+    "dense_matrix",
+    "gebrd_blocked",
+    "gebrd_unblocked",
+    "geqrf_blocked",
+    "gesdd",
+    "gesdd_batched",
+    "labrd_panel",
+    "launch_count",
+    "matmul_accumulate",
+    "matvec_accumulate",
+    "orgqr",
+    "ormlq_like",
+    "ormqr_like",
+    "phase_profile",
+    "row_reflectors",
+    "svd",
+]

@@ -1,0 +1,209 @@
+"""ctypes binding of libdcsvd_b200.so (C ABI in include/dcsvd_b200.h).
+
+This is the only place Python touches the native library.  There is no
+fallback: if the shared library or a CUDA device is missing, every entry
+point raises.  PyTorch provides device memory and the current stream.
+"""
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdcsvd_b200.so")
+
+# status codes (include/dcsvd_b200.h)
+OK, EINVAL, ENOCONV, EARITH, ESINGULAR, ECUDA = range(6)
+
+EXPORTED = (
+    "dcsvd_create", "dcsvd_destroy", "dcsvd_last_error", "dcsvd_version", "dcsvd_launch_count",
+    "dcsvd_dgemm", "dcsvd_dgemv", "dcsvd_gebrd", "dcsvd_labrd", "dcsvd_bdsdc", "dcsvd_geqrf",
+    "dcsvd_orgqr", "dcsvd_ormbr", "dcsvd_gesdd", "dcsvd_gesdd_batched",
+)
+
+
+class ConvergenceError(RuntimeError):
+    """An iterative kernel exceeded its iteration budget
+    (pkg/src/dcsvd/densecore.py:29-30)."""
+
+
+class DcsvdOpts(ctypes.Structure):
+    _fields_ = [
+        ("want_vectors", ctypes.c_int),
+        ("bidiag_block", ctypes.c_int),
+        ("qr_block", ctypes.c_int),
+        ("orgqr_block", ctypes.c_int),
+        ("apply_block", ctypes.c_int),
+        ("leaf_size", ctypes.c_int),
+        ("ts_crossover", ctypes.c_double),
+        ("deflation_multiple", ctypes.c_double),
+    ]
+
+
+class DcsvdPhaseTimes(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in ("geqrf", "orgqr", "gebrd", "bdcdc", "ormbr", "gemm", "total")]
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library(path=None):
+    """Load (once) and prototype the native library.  Raises if absent."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        p = path or LIB_PATH
+        if not os.path.exists(p):
+            raise RuntimeError(
+                f"libdcsvd_b200.so not found at {p}; build it with "
+                "`python -m paper_2508_11467_b200.build` (no CPU fallback exists)"
+            )
+        lib = ctypes.CDLL(p)
+        V, I, I64, D, C = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_char
+        proto = {
+            "dcsvd_create": (I, [ctypes.POINTER(V), I]),
+            "dcsvd_destroy": (I, [V]),
+            "dcsvd_last_error": (ctypes.c_char_p, [V]),
+            "dcsvd_version": (I, []),
+            "dcsvd_launch_count": (ctypes.c_longlong, [V]),
+            "dcsvd_dgemm": (I, [V, I, I, I64, I64, I64, D, V, I64, V, I64, D, V, I64, V]),
+            "dcsvd_dgemv": (I, [V, I, I64, I64, D, V, I64, V, D, V, V]),
+            "dcsvd_gebrd": (I, [V, I64, I64, V, I64, V, V, V, V, I, V]),
+            "dcsvd_labrd": (I, [V, I64, I64, V, I64, V, V, V, V, I, V, I64, V, I64, V]),
+            "dcsvd_bdsdc": (I, [V, I64, V, V, I, I, I, D, V, V, I64, V, I64, V, V]),
+            "dcsvd_geqrf": (I, [V, I64, I64, V, I64, V, I, V]),
+            "dcsvd_orgqr": (I, [V, I64, I64, I64, V, I64, V, V, I64, I, V]),
+            "dcsvd_ormbr": (I, [V, C, I, I64, I64, V, I64, V, V, I64, I64, I64, I, V]),
+            "dcsvd_gesdd": (I, [V, I64, I64, V, I64, V, V, I64, V, I64, ctypes.POINTER(DcsvdOpts),
+                                ctypes.POINTER(DcsvdPhaseTimes), V]),
+            "dcsvd_gesdd_batched": (I, [V, I, I64, I64, ctypes.POINTER(V), I64, ctypes.POINTER(V),
+                                        ctypes.POINTER(V), I64, ctypes.POINTER(V), I64,
+                                        ctypes.POINTER(DcsvdOpts), I, V]),
+        }
+        for name, (res, args) in proto.items():
+            f = getattr(lib, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = lib
+        return lib
+
+
+_handles = {}
+_handles_lock = threading.Lock()
+
+
+def handle(device=None):
+    """Per-(thread, device) library handle."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2508_11467_b200 requires a CUDA device (B200); no CPU fallback exists")
+    lib = load_library()
+    dev = torch.cuda.current_device() if device is None else int(device)
+    key = (threading.get_ident(), dev)
+    with _handles_lock:
+        h = _handles.get(key)
+        if h is None:
+            hv = ctypes.c_void_p()
+            rc = lib.dcsvd_create(ctypes.byref(hv), dev)
+            if rc != 0:
+                raise RuntimeError(f"dcsvd_create failed on device {dev} (status {rc})")
+            h = hv
+            _handles[key] = h
+    return h
+
+
+def check(rc, h):
+    if rc == OK:
+        return
+    msg = load_library().dcsvd_last_error(h).decode(errors="replace")
+    if rc == EINVAL:
+        raise ValueError(msg)
+    if rc == ENOCONV:
+        raise ConvergenceError(msg)
+    if rc == EARITH:
+        raise ArithmeticError(msg)
+    if rc == ESINGULAR:
+        raise np.linalg.LinAlgError(msg)
+    raise RuntimeError(msg)
+
+
+def stream_ptr():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def launch_count():
+    return int(load_library().dcsvd_launch_count(None))
+
+
+# ---------------------------------------------------------------------------
+# array plumbing: column-major fp64 device tensors
+
+
+def colmajor_empty(m, n, device=None):
+    """m x n float64 CUDA tensor with column-major strides (1, m)."""
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    return torch.empty((n, m), dtype=torch.float64, device=dev).t()
+
+
+def is_colmajor(t):
+    return t.dim() == 2 and t.stride(0) == 1 and (t.shape[1] <= 1 or t.stride(1) >= max(t.shape[0], 1))
+
+
+def to_device_colmajor(x, copy=True):
+    """Return (tensor, was_numpy).  numpy input is copied to the current CUDA
+    device; torch input keeps its memory unless it must be re-laid-out (or
+    ``copy``)."""
+    if isinstance(x, torch.Tensor):
+        if x.dim() != 2:
+            raise ValueError(f"expected a 2-d array, got ndim={x.dim()}")
+        t = x
+        if not t.is_cuda:
+            t = t.to("cuda")
+        if t.dtype != torch.float64:
+            t = t.to(torch.float64)
+        if copy or not is_colmajor(t):
+            c = colmajor_empty(t.shape[0], t.shape[1], t.device.index)
+            c.copy_(t)
+            t = c
+        return t, False
+    a = np.asarray(x, dtype=np.float64)
+    if a.ndim != 2:
+        raise ValueError(f"expected a 2-d array, got ndim={a.ndim}")
+    m, n = a.shape
+    t = colmajor_empty(m, n)
+    # a.T as C-contiguous == a in Fortran order; copy through a pinned staging tensor
+    host = torch.from_numpy(np.ascontiguousarray(a.T))
+    t.t().copy_(host, non_blocking=False)
+    return t, True
+
+
+def vec_to_device(v, n=None):
+    if isinstance(v, torch.Tensor):
+        t = v.to(device="cuda", dtype=torch.float64).contiguous()
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(v, dtype=np.float64))).to("cuda")
+    if n is not None and t.numel() != n:
+        raise ValueError(f"expected {n} entries, got {t.numel()}")
+    return t
+
+
+def to_host(t):
+    """Device tensor -> numpy (Fortran order for matrices)."""
+    if t is None:
+        return None
+    if t.dim() == 2:
+        return np.asfortranarray(t.t().contiguous().cpu().numpy().T)
+    return t.cpu().numpy()
+
+
+def ptr(t):
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def ld(t):
+    """Leading dimension of a column-major 2-d tensor."""
+    return max(int(t.stride(1)), max(int(t.shape[0]), 1)) if t.shape[1] > 1 else max(int(t.shape[0]), 1)

@@ -1,0 +1,419 @@
+// C ABI of libdcsvd_b200 (include/dcsvd_b200.h) and the gesdd driver.
+//
+// Driver reference: pkg/src/dcsvd/driver.py:97-170 (_square_core,
+// _gesdd_impl, gesdd, phase_profile).
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <atomic>
+#include <mutex>
+
+#include "ctx.cuh"
+#include "gemm.cuh"
+#include "launch.cuh"
+
+namespace dc {
+std::atomic<long long> g_launch_count{0};
+thread_local dcsvd_ctx* t_cur = nullptr;
+
+int set_error(dcsvd_ctx* h, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (h) h->last_error = buf;
+  return code;
+}
+
+int pool_reserve(dcsvd_ctx* h, int p, size_t bytes, cudaStream_t st) {
+  DevPool& pl = h->pool[p];
+  pl.used = 0;
+  if (bytes <= pl.cap) return 0;
+  if (pl.ptr) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return set_error(h, DCSVD_ECUDA, "CUDA error before regrow: %s", cudaGetErrorString(e));
+    cudaFree(pl.ptr);
+    pl.ptr = nullptr;
+    pl.cap = 0;
+  }
+  size_t cap = bytes + bytes / 8 + (1 << 20);
+  cudaError_t e = cudaMalloc(&pl.ptr, cap);
+  if (e != cudaSuccess) {
+    pl.ptr = nullptr;
+    return set_error(h, DCSVD_ECUDA, "cudaMalloc(%zu) failed: %s", cap, cudaGetErrorString(e));
+  }
+  pl.cap = cap;
+  return 0;
+}
+
+int check_device_status(dcsvd_ctx* h, cudaStream_t st, const char* stage) {
+  cudaError_t e = cudaMemcpyAsync(h->h_err, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return set_error(h, DCSVD_ECUDA, "%s: CUDA error %s", stage, cudaGetErrorString(e));
+  const int code = *h->h_err;
+  if (code == kDevOk) return 0;
+  cudaMemsetAsync(h->d_err, 0, sizeof(int), st);
+  switch (code) {
+    case kDevNoConvergeQR:
+      return set_error(h, DCSVD_ENOCONV, "%s: bidiagonal QR iteration exceeded its rotation budget", stage);
+    case kDevNoConvergeSecular:
+      return set_error(h, DCSVD_ENOCONV, "%s: secular solver did not converge in 100 iterations", stage);
+    case kDevInterlacing:
+      return set_error(h, DCSVD_EARITH, "%s: root interlacing violated: non-positive radicand in z update", stage);
+    case kDevSingularT:
+      return set_error(h, DCSVD_ESINGULAR, "%s: triangular factor has a zero diagonal entry", stage);
+    default:
+      return set_error(h, DCSVD_EINVAL, "%s: device status %d", stage, code);
+  }
+}
+}  // namespace dc
+
+int dc_cuda_fail(cudaError_t e, const char* what) {
+  if (dc::t_cur) dc::set_error(dc::t_cur, DCSVD_ECUDA, "CUDA error %s in %s", cudaGetErrorString(e), what);
+  return DCSVD_ECUDA;
+}
+
+using namespace dc;
+
+namespace {
+struct Guard {
+  Guard(dcsvd_ctx* h) {
+    t_cur = h;
+    if (h) cudaSetDevice(h->device);
+  }
+  ~Guard() { t_cur = nullptr; }
+};
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+__global__ void transpose_kernel(int rows, int cols, const double* __restrict__ A, long long lda, double* __restrict__ B,
+                                 long long ldb) {
+  // B (cols x rows) = A^T
+  __shared__ double tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int k = ty; k < 32; k += 8) {
+    const int r = bx + tx, c = by + k;
+    tile[k][tx] = (r < rows && c < cols) ? A[r + (long long)c * lda] : 0.0;
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int r = bx + k, c = by + tx;
+    if (r < rows && c < cols) B[c + (long long)r * ldb] = tile[tx][k];
+  }
+}
+int transpose(cudaStream_t st, int rows, int cols, const double* A, long long lda, double* B, long long ldb) {
+  if (rows <= 0 || cols <= 0) return 0;
+  transpose_kernel<<<dim3((rows + 31) / 32, (cols + 31) / 32), 256, 0, st>>>(rows, cols, A, lda, B, ldb);
+  note_launch();
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+__global__ void triu_copy_kernel(int n, const double* __restrict__ A, long long lda, double* __restrict__ R,
+                                 long long ldr) {
+  const long long total = (long long)n * n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx % n), j = (int)(idx / n);
+    R[i + (long long)j * ldr] = i <= j ? A[i + (long long)j * lda] : 0.0;
+  }
+}
+
+struct PhaseTimer {
+  bool on;
+  cudaStream_t st;
+  cudaEvent_t ev[16];
+  int idx[16];
+  int cnt = 0;
+  PhaseTimer(bool on_, cudaStream_t s) : on(on_), st(s) {}
+  ~PhaseTimer() {
+    for (int i = 0; i < cnt; ++i) cudaEventDestroy(ev[i]);
+  }
+  void mark(int phase) {  // phase = index into the profile struct (0..5), -1 = end marker
+    if (!on || cnt >= 16) return;
+    cudaEventCreate(&ev[cnt]);
+    cudaEventRecord(ev[cnt], st);
+    idx[cnt] = phase;
+    ++cnt;
+  }
+  void collect(dcsvd_phase_times* p) {
+    if (!on || !p) return;
+    double* f[6] = {&p->geqrf, &p->orgqr, &p->gebrd, &p->bdcdc, &p->ormbr, &p->gemm};
+    for (int i = 0; i + 1 < cnt; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      if (idx[i] >= 0) *f[idx[i]] += ms * 1e-3;
+    }
+    if (cnt >= 2) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[0], ev[cnt - 1]);
+      p->total = ms * 1e-3;
+    }
+  }
+};
+enum { PH_GEQRF = 0, PH_ORGQR, PH_GEBRD, PH_BDC, PH_ORMBR, PH_GEMM, PH_END = -1 };
+
+// _square_core (driver.py:97-118) for m >= n.  A consumed.
+int square_core(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A, long long lda, double* S,
+                double* U, long long ldu, double* VT, long long ldvt, const dcsvd_opts& o, PhaseTimer& pt,
+                double* dbuf) {
+  double* d = dbuf;
+  double* e = d + n;
+  double* tq = e + n;
+  double* tp = tq + n;
+  pt.mark(PH_GEBRD);
+  int rc = gebrd_run(h, st, m, n, A, lda, d, e, tq, tp, o.bidiag_block);
+  if (rc) return rc;
+  pt.mark(PH_BDC);
+  const bool vec = o.want_vectors != 0;
+  rc = bdsdc_run(h, st, n, d, e, false, vec, o.leaf_size, o.deflation_multiple, S, nullptr, vec ? U : nullptr, ldu,
+                 m, nullptr, 0, vec ? VT : nullptr, ldvt);
+  if (rc) return rc;
+  if (!vec) return 0;
+  pt.mark(PH_ORMBR);
+  rc = ormbr_run(h, st, 'Q', false, m, n, A, lda, tq, U, m, n, ldu, o.apply_block);
+  if (rc) return rc;
+  rc = ormbr_run(h, st, 'P', true, m, n, A, lda, tp, VT, n, n, ldvt, o.apply_block);
+  return rc;
+}
+
+int gesdd_tall(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A, long long lda, double* S,
+               double* U, long long ldu, double* VT, long long ldvt, const dcsvd_opts& o, PhaseTimer& pt) {
+  const bool vec = o.want_vectors != 0;
+  const bool ts = (double)m >= o.ts_crossover * (double)n && m > n;
+  size_t need = pool_bytes(4 * n + 8, 8);
+  if (ts) need += pool_bytes(n, 8) + pool_bytes((size_t)n * n, 8) + (vec ? pool_bytes((size_t)n * n, 8) + pool_bytes((size_t)m * n, 8) : 0);
+  int rc = pool_reserve(h, 1, need, st);
+  if (rc) return rc;
+  double* dbuf = pool_take<double>(h, 1, 4 * n + 8);
+  if (!ts) return square_core(h, st, m, n, A, lda, S, U, ldu, VT, ldvt, o, pt, dbuf);
+  // TS path (driver.py:132-143)
+  double* tau = pool_take<double>(h, 1, n);
+  double* R = pool_take<double>(h, 1, (size_t)n * n);
+  double* U0 = vec ? pool_take<double>(h, 1, (size_t)n * n) : nullptr;
+  double* Qm = vec ? pool_take<double>(h, 1, (size_t)m * n) : nullptr;
+  pt.mark(PH_GEQRF);
+  rc = geqrf_run(h, st, m, n, A, lda, tau, o.qr_block);
+  if (rc) return rc;
+  triu_copy_kernel<<<std::min<long long>(148 * 8, (n * n + 255) / 256), 256, 0, st>>>((int)n, A, lda, R, n);
+  note_launch();
+  rc = square_core(h, st, n, n, R, n, S, U0, n, VT, ldvt, o, pt, dbuf);
+  if (rc || !vec) return rc;
+  pt.mark(PH_ORGQR);
+  rc = orgqr_run(h, st, m, n, n, A, lda, tau, Qm, m, o.orgqr_block);
+  if (rc) return rc;
+  pt.mark(PH_GEMM);
+  GemmDesc g;
+  g.m = (int)m; g.n = (int)n; g.k = (int)n;
+  g.A = Qm; g.lda = m; g.acol = nullptr;
+  g.B = U0; g.ldb = n;
+  g.C = U; g.ldc = ldu; g.ccol = nullptr;
+  g.alpha = 1.0; g.beta = 0.0;
+  return gemm_launch(st, false, false, g);
+}
+
+int validate_opts(dcsvd_ctx* h, const dcsvd_opts& o) {
+  if (o.bidiag_block < 1 || o.qr_block < 1 || o.orgqr_block < 1 || o.apply_block < 1 || o.leaf_size < 1)
+    return set_error(h, DCSVD_EINVAL, "block sizes must be >= 1");
+  if (!(o.ts_crossover >= 1.0)) return set_error(h, DCSVD_EINVAL, "ts_crossover must be >= 1");
+  if (!(o.deflation_multiple > 0.0)) return set_error(h, DCSVD_EINVAL, "deflation_multiple must be > 0");
+  return 0;
+}
+
+dcsvd_opts default_opts() {
+  dcsvd_opts o;
+  o.want_vectors = 1; o.bidiag_block = 32; o.qr_block = 32; o.orgqr_block = 64; o.apply_block = 64;
+  o.leaf_size = 32; o.ts_crossover = 5.0 / 3.0; o.deflation_multiple = 8.0;
+  return o;
+}
+
+int gesdd_impl(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A, long long lda, double* S,
+               double* U, long long ldu, double* VT, long long ldvt, const dcsvd_opts& o, PhaseTimer& pt) {
+  if (m < 1 || n < 1) return set_error(h, DCSVD_EINVAL, "matrix must be nonempty, got %lldx%lld", m, n);
+  if (m >= n) return gesdd_tall(h, st, m, n, A, lda, S, U, ldu, VT, ldvt, o, pt);
+  // wide: SVD of A^T (driver.py:125-131)
+  const bool vec = o.want_vectors != 0;
+  // At (n x m), U' (n x m), VT' (m x m) live in pool 1's tail: reserve separately
+  // through a dedicated allocation (pool 1 is re-reserved by gesdd_tall).
+  double *At = nullptr, *Up = nullptr, *VTp = nullptr;
+  size_t bytes = sizeof(double) * ((size_t)n * m + (vec ? (size_t)n * m + (size_t)m * m : 0));
+  char* blk = nullptr;
+  DC_CUDA_TRY(cudaMallocAsync((void**)&blk, bytes, st));
+  At = (double*)blk;
+  if (vec) {
+    Up = At + (size_t)n * m;
+    VTp = Up + (size_t)n * m;
+  }
+  int rc = transpose(st, (int)m, (int)n, A, lda, At, n);
+  if (!rc) rc = gesdd_tall(h, st, n, m, At, n, S, Up, n, VTp, m, o, pt);
+  if (!rc && vec) {
+    rc = transpose(st, (int)m, (int)m, VTp, m, U, ldu);          // U = VT'^T (m x m)
+    if (!rc) rc = transpose(st, (int)n, (int)m, Up, n, VT, ldvt);  // VT = U'^T (m x n)
+  }
+  cudaFreeAsync(blk, st);
+  return rc;
+}
+}  // namespace
+
+extern "C" {
+
+int dcsvd_version(void) { return 100; }
+
+int dcsvd_create(dcsvd_handle* out, int device) {
+  if (!out) return DCSVD_EINVAL;
+  *out = nullptr;
+  dcsvd_ctx* h = new dcsvd_ctx();
+  h->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete h;
+    return DCSVD_ECUDA;
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+    delete h;
+    return DCSVD_ECUDA;
+  }
+  h->sms = prop.multiProcessorCount;
+  h->coop_ok = prop.cooperativeLaunch;
+  if (cudaMalloc(&h->d_err, sizeof(int)) != cudaSuccess || cudaMalloc(&h->d_bar, sizeof(unsigned) * kNumBars) != cudaSuccess ||
+      cudaMallocHost(&h->h_err, sizeof(int)) != cudaSuccess) {
+    delete h;
+    return DCSVD_ECUDA;
+  }
+  cudaMemset(h->d_err, 0, sizeof(int));
+  cudaMemset(h->d_bar, 0, sizeof(unsigned) * kNumBars);
+  cudaDeviceSynchronize();
+  *out = h;
+  return 0;
+}
+
+int dcsvd_destroy(dcsvd_handle h) {
+  if (!h) return 0;
+  cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  for (auto& p : h->pool)
+    if (p.ptr) cudaFree(p.ptr);
+  cudaFree(h->d_err);
+  cudaFree(h->d_bar);
+  cudaFreeHost(h->h_err);
+  delete h;
+  return 0;
+}
+
+const char* dcsvd_last_error(dcsvd_handle h) { return h ? h->last_error.c_str() : "null handle"; }
+
+long long dcsvd_launch_count(dcsvd_handle) { return g_launch_count.load(); }
+
+int dcsvd_dgemm(dcsvd_handle h, int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
+                int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  if (m < 0 || n < 0 || k < 0) return set_error(h, DCSVD_EINVAL, "negative GEMM dimension");
+  if (m == 0 || n == 0) return 0;
+  GemmDesc d;
+  d.m = (int)m; d.n = (int)n; d.k = (int)k;
+  d.A = A; d.lda = lda; d.acol = nullptr;
+  d.B = B; d.ldb = ldb;
+  d.C = C; d.ldc = ldc; d.ccol = nullptr;
+  d.alpha = alpha; d.beta = beta;
+  return gemm_launch(S(stream), transa != 0, transb != 0, d);
+}
+
+int dcsvd_dgemv(dcsvd_handle h, int transa, int64_t m, int64_t n, double alpha, const double* A, int64_t lda,
+                const double* x, double beta, double* y, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  return gemv_launch(S(stream), transa != 0, (int)m, (int)n, alpha, A, lda, x, beta, y);
+}
+
+int dcsvd_gebrd(dcsvd_handle h, int64_t m, int64_t n, double* A, int64_t lda, double* d, double* e, double* tauq,
+                double* taup, int nb, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  return gebrd_run(h, S(stream), m, n, A, lda, d, e, tauq, taup, nb);
+}
+
+int dcsvd_labrd(dcsvd_handle h, int64_t m, int64_t n, double* A, int64_t lda, double* d, double* e, double* tauq,
+                double* taup, int nb, double* P, int64_t ldp, double* Q, int64_t ldq, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  return labrd_run(h, S(stream), m, n, A, lda, nb, d, e, tauq, taup, P, ldp, Q, ldq);
+}
+
+int dcsvd_bdsdc(dcsvd_handle h, int64_t n, const double* d, const double* e, int bordered, int want_vectors, int leaf,
+                double tol_multiple, double* dvals, double* W, int64_t ldw, double* Q, int64_t ldq, double* edge,
+                void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  cudaStream_t st = S(stream);
+  int rc = bdsdc_run(h, st, n, d, e, bordered != 0, want_vectors != 0, leaf, tol_multiple, dvals, edge,
+                     want_vectors ? W : nullptr, ldw, n, want_vectors ? Q : nullptr, ldq, nullptr, 0);
+  if (rc) return rc;
+  return check_device_status(h, st, "bdsdc");
+}
+
+int dcsvd_geqrf(dcsvd_handle h, int64_t m, int64_t n, double* A, int64_t lda, double* tau, int nb, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  return geqrf_run(h, S(stream), m, n, A, lda, tau, nb);
+}
+
+int dcsvd_orgqr(dcsvd_handle h, int64_t m, int64_t nrefl, int64_t k, const double* A, int64_t lda, const double* tau,
+                double* Q, int64_t ldq, int nb, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  int rc = orgqr_run(h, S(stream), m, nrefl, k, A, lda, tau, Q, ldq, nb);
+  if (rc) return rc;
+  return check_device_status(h, S(stream), "orgqr");
+}
+
+int dcsvd_ormbr(dcsvd_handle h, char vect, int trans, int64_t m, int64_t n, const double* A, int64_t lda,
+                const double* tau, double* C, int64_t c_rows, int64_t c_cols, int64_t ldc, int nb, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  int rc = ormbr_run(h, S(stream), vect, trans != 0, m, n, A, lda, tau, C, c_rows, c_cols, ldc, nb);
+  if (rc) return rc;
+  return check_device_status(h, S(stream), "ormbr");
+}
+
+int dcsvd_gesdd(dcsvd_handle h, int64_t m, int64_t n, double* A, int64_t lda, double* Sg, double* U, int64_t ldu,
+                double* VT, int64_t ldvt, const dcsvd_opts* opts, dcsvd_phase_times* prof, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  dcsvd_opts o = opts ? *opts : default_opts();
+  int rc = validate_opts(h, o);
+  if (rc) return rc;
+  cudaStream_t st = S(stream);
+  if (prof) *prof = dcsvd_phase_times{0, 0, 0, 0, 0, 0, 0};
+  PhaseTimer pt(prof != nullptr, st);
+  pt.mark(PH_END);
+  rc = gesdd_impl(h, st, m, n, A, lda, Sg, U, ldu, VT, ldvt, o, pt);
+  pt.mark(PH_END);
+  if (rc) return rc;
+  rc = check_device_status(h, st, "gesdd");
+  if (rc) return rc;
+  pt.collect(prof);
+  return 0;
+}
+
+int dcsvd_gesdd_batched(dcsvd_handle h, int batch, int64_t m, int64_t n, double* const* A, int64_t lda,
+                        double* const* Sg, double* const* U, int64_t ldu, double* const* VT, int64_t ldvt,
+                        const dcsvd_opts* opts, int concurrency, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  dcsvd_opts o = opts ? *opts : default_opts();
+  int rc = validate_opts(h, o);
+  if (rc) return rc;
+  cudaStream_t st = S(stream);
+  (void)concurrency;
+  for (int b = 0; b < batch; ++b) {
+    PhaseTimer pt(false, st);
+    rc = gesdd_impl(h, st, m, n, A[b], lda, Sg[b], U ? U[b] : nullptr, ldu, VT ? VT[b] : nullptr, ldvt, o, pt);
+    if (rc) return rc;
+  }
+  return check_device_status(h, st, "gesdd_batched");
+}
+
+}  // extern "C"

@@ -1,0 +1,69 @@
+// Handle state: device, scratch pools, status word, barrier counters.
+#pragma once
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+struct DevPool {
+  char* ptr = nullptr;
+  size_t cap = 0;
+  size_t used = 0;
+};
+
+struct dcsvd_ctx {
+  int device = 0;
+  int sms = 148;
+  int coop_ok = 1;
+  std::string last_error;
+  int* d_err = nullptr;         // device status word (dc::DevErr)
+  unsigned* d_bar = nullptr;    // grid-barrier counters (kNumBars)
+  int* h_err = nullptr;         // pinned mirror of d_err
+  DevPool pool[3];              // 0: stage scratch, 1: driver buffers, 2: bdc
+};
+
+namespace dc {
+constexpr int kNumBars = 64;
+
+// Ensure pool `p` holds at least `bytes` (synchronizes `st` before a regrow so
+// in-flight kernels never see a freed buffer), reset its bump pointer.
+int pool_reserve(dcsvd_ctx* h, int p, size_t bytes, cudaStream_t st);
+// Carve `count` doubles (256-byte aligned) from pool `p`.
+template <typename T>
+inline T* pool_take(dcsvd_ctx* h, int p, size_t count) {
+  DevPool& pl = h->pool[p];
+  size_t bytes = (count * sizeof(T) + 255) & ~size_t(255);
+  if (pl.used + bytes > pl.cap) return nullptr;
+  T* r = reinterpret_cast<T*>(pl.ptr + pl.used);
+  pl.used += bytes;
+  return r;
+}
+inline size_t pool_bytes(size_t count, size_t elem) { return (count * elem + 255) & ~size_t(255); }
+
+int set_error(dcsvd_ctx* h, int code, const char* fmt, ...);
+// Read and reset the device status word (synchronizes the stream); maps it
+// to an API status code with a message.
+int check_device_status(dcsvd_ctx* h, cudaStream_t st, const char* stage);
+
+// stage entry points (all stream-ordered on `st`)
+int gebrd_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A, long long lda,
+              double* d, double* e, double* tauq, double* taup, int nb);
+int labrd_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A, long long lda, int nb, double* d,
+              double* e, double* tauq, double* taup, double* P, long long ldp, double* Q, long long ldq);
+int geqrf_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A, long long lda,
+              double* tau, int nb);
+int orgqr_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long nrefl, long long k, const double* A,
+              long long lda, const double* tau, double* Q, long long ldq, int nb);
+// Left apply of column reflectors stored below the diagonal of A (rows >= j of
+// reflector j, offset `roff` = 0) or right apply of row reflectors stored right
+// of the superdiagonal (offset 1).  See qr.cu.
+int ormbr_run(dcsvd_ctx* h, cudaStream_t st, char vect, bool trans, long long m, long long n,
+              const double* A, long long lda, const double* tau, double* C, long long c_rows,
+              long long c_cols, long long ldc, int nb);
+// Bidiagonal D&C.  Outputs (all optional except dvals): edge_out (2 x ncols),
+// Wout = [W_desc; 0] with wrows >= n rows, Qout (ncols x ncols), VT = Q_desc^T
+// (n x n, square problems).
+int bdsdc_run(dcsvd_ctx* h, cudaStream_t st, long long n, const double* d, const double* e, bool bordered,
+              bool vectors, int leaf, double tol_mult, double* dvals, double* edge_out, double* Wout,
+              long long ldwo, long long wrows, double* Qout, long long ldqo, double* VT, long long ldvt);
+}  // namespace dc

@@ -1,0 +1,528 @@
+// One-stage bidiagonalization (GEBRD) on the GPU.
+//
+// Reference: pkg/src/dcsvd/bidiag.py:113-204 (merged rank-2b LABRD panel +
+// single trailing GEMM), arxiv 2508.11467 Alg. 1.
+//
+// Design: one persistent cooperative kernel per panel.
+// Each column step is five phases separated by four grid barriers:
+//   P1/P5  column update  c = a[k:,k] - P[k:,:2k] Q[k,:2k]   (1-D over rows)
+//   P2     LARFG(col) + partial A^T v (2-D blocks) + partial P^T v
+//   P3     y = tau (A^T v - Q (P^T v)), row update, row norm   (1-D over cols)
+//   P4     LARFG(row) + partial A u (2-D blocks) + partial Q^T u
+//   P5     x = pi (A u - P (Q^T u)), fused with the next column update.
+// The two big GEMVs read the panel-start trailing matrix (untouched until the
+// trailing update), so the A u pass walks each CTA's block in the opposite
+// column order of the A^T v pass: the tail of one pass is still in L2 when
+// the next one starts ("snake").  All reductions use fixed trees / fixed
+// partial order (bit-reproducible).  The trailing update A -= P Q^T is one
+// DMMA GEMM (gemm.cu).  The final <= nb columns use a single-CTA GEBD2.
+#include <cooperative_groups.h>
+
+#include "ctx.cuh"
+#include "gemm.cuh"
+#include "launch.cuh"
+
+namespace dc {
+
+struct LabrdArgs {
+  double* A;
+  long long lda;
+  int m, n, nb;
+  double* P;
+  double* Q;
+  long long ldp, ldq;
+  double *d, *e, *tauq, *taup;
+  double *cvec, *rvec, *normc, *normr, *py, *px, *pw, *ps;
+  long long ldpy, ldpx;  // leading dims of py (>= n) and px (>= m)
+  unsigned* bar;
+  int Gr, Gc, RB, CB, R1, C1;
+};
+
+constexpr int kLabrdThreads = 512;
+constexpr int kLabrdWarps = kLabrdThreads / 32;
+
+// Sum of `cnt` partials in fixed order by a fixed block tree.
+__device__ __forceinline__ double sum_partials(const double* p, int cnt, double* sh) {
+  double v = 0.0;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) v += p[i];
+  return block_sum(v, sh);
+}
+
+__device__ __forceinline__ void larfg_scalars(double alpha, double nrm2, double& tau, double& beta) {
+  const double xn = sqrt(nrm2);
+  if (xn == 0.0) {
+    tau = 0.0;
+    beta = alpha;
+  } else {
+    beta = -copysign(hypot(alpha, xn), alpha);
+    tau = (beta - alpha) / beta;
+  }
+}
+
+template <int RPL>
+__global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
+  extern __shared__ double dsm[];
+  __shared__ double sh_red[32];
+  __shared__ double sh_coef[64];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = blockIdx.x;
+  const int G = gridDim.x;
+  const int gr = g % a.Gr, gc = g / a.Gr;
+  const int m = a.m, n = a.n, nb = a.nb;
+  double* __restrict__ A = a.A;
+  const long long lda = a.lda, ldp = a.ldp, ldq = a.ldq;
+  double* __restrict__ P = a.P;
+  double* __restrict__ Q = a.Q;
+  unsigned epoch = 0;
+  // 2-D block of this CTA
+  const int br0 = gr * a.RB, br1 = min(m, br0 + a.RB);
+  const int bc0 = gc * a.CB, bc1 = min(n, bc0 + a.CB);
+  // 1-D slices
+  const int r1lo = g * a.R1, r1hi = min(m, r1lo + a.R1);
+  const int c1lo = g * a.C1, c1hi = min(n, c1lo + a.C1);
+  double* sh_u = dsm;                         // CB doubles
+  double* sh_acc = dsm + ((a.CB + 1) & ~1);   // kLabrdWarps * RB doubles
+
+  // ---- phase 1 for k = 0: c = a[:,0]
+  {
+    double part = 0.0;
+    const int r = r1lo + tid;
+    if (tid < a.R1 && r < r1hi) {
+      const double c = A[r];
+      a.cvec[r] = c;
+      if (r > 0) part = c * c;
+    }
+    part = block_sum(part, sh_red);
+    if (tid == 0) a.normc[g] = part;
+  }
+  grid_barrier(a.bar, G, epoch);
+
+  for (int k = 0; k < nb; ++k) {
+    const int c0 = 2 * k, c1 = 2 * k + 1;
+    // ================= phase 2: LARFG(col), A^T v, P^T v
+    double tau, beta;
+    const double alpha = a.cvec[k];
+    larfg_scalars(alpha, sum_partials(a.normc, G, sh_red), tau, beta);
+    const double den = alpha - beta;
+    if (g == 0 && tid == 0) {
+      a.d[k] = beta;
+      a.tauq[k] = tau;
+      A[k + (long long)k * lda] = beta;
+      P[k + (long long)c0 * ldp] = 1.0;
+    }
+    {
+      const int r = r1lo + tid;
+      if (tid < a.R1 && r < r1hi && r > k) {
+        const double c = a.cvec[r];
+        const double ess = tau != 0.0 ? c / den : c;
+        A[r + (long long)k * lda] = ess;
+        P[r + (long long)c0 * ldp] = ess;
+      }
+    }
+    if (tau != 0.0) {
+      double v[RPL];
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int r = br0 + lane + 32 * i;
+        v[i] = (r < br1 && r >= k) ? (r == k ? 1.0 : a.cvec[r] / den) : 0.0;
+      }
+      const int jstart = max(bc0, k + 1);
+      for (int j = jstart + warp; j < bc1; j += kLabrdWarps) {
+        const double* col = A + (long long)j * lda;
+        double x[RPL];
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) {
+          const int r = br0 + lane + 32 * i;
+          x[i] = r < br1 ? col[r] : 0.0;
+        }
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) s += x[i] * v[i];
+        s = warp_sum(s);
+        if (lane == 0) a.py[(long long)gr * a.ldpy + j] = s;
+      }
+      // P^T v over this block's rows for t = gc, gc+Gc, ... < 2k
+      for (int t = gc + a.Gc * warp; t < c0; t += a.Gc * kLabrdWarps) {
+        const double* pc = P + (long long)t * ldp;
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) {
+          const int r = br0 + lane + 32 * i;
+          if (r < br1) s += pc[r] * v[i];
+        }
+        s = warp_sum(s);
+        if (lane == 0) a.pw[gr * 64 + t] = s;
+      }
+    }
+    grid_barrier(a.bar, G, epoch);
+
+    // ================= phase 3: y, row update, row norm partial
+    if (tau != 0.0 && tid < c0) {
+      double s = 0.0;
+      for (int q = 0; q < a.Gr; ++q) s += a.pw[q * 64 + tid];
+      sh_coef[tid] = s;
+    }
+    __syncthreads();
+    {
+      double part = 0.0;
+      const int j = c1lo + tid;
+      if (tid < a.C1 && j < c1hi && j > k) {
+        double y = 0.0;
+        if (tau != 0.0) {
+          double s = 0.0;
+          for (int q = 0; q < a.Gr; ++q) s += a.py[(long long)q * a.ldpy + j];
+          double corr = 0.0;
+          for (int t = 0; t < c0; ++t) corr += Q[j + (long long)t * ldq] * sh_coef[t];
+          y = tau * (s - corr);
+          Q[j + (long long)c0 * ldq] = y;
+        }
+        double upd = 0.0;
+        for (int t = 0; t < c0; ++t) upd += Q[j + (long long)t * ldq] * P[k + (long long)t * ldp];
+        upd += y;  // Q[j,2k] * P[k,2k] with P[k,2k] = 1
+        const double r = A[k + (long long)j * lda] - upd;
+        A[k + (long long)j * lda] = r;
+        a.rvec[j] = r;
+        if (j > k + 1) part = r * r;
+      }
+      part = block_sum(part, sh_red);
+      if (tid == 0) a.normr[g] = part;
+    }
+    grid_barrier(a.bar, G, epoch);
+
+    // ================= phase 4: LARFG(row), A u, Q^T u
+    double pi, betar;
+    const double alr = a.rvec[k + 1];
+    larfg_scalars(alr, sum_partials(a.normr, G, sh_red), pi, betar);
+    const double denr = alr - betar;
+    if (g == 0 && tid == 0) {
+      a.e[k] = betar;
+      a.taup[k] = pi;
+      A[k + (long long)(k + 1) * lda] = betar;
+      Q[(k + 1) + (long long)c1 * ldq] = 1.0;
+    }
+    {
+      const int j = c1lo + tid;
+      if (tid < a.C1 && j < c1hi && j > k + 1) {
+        const double rv = a.rvec[j];
+        const double ess = pi != 0.0 ? rv / denr : rv;
+        A[k + (long long)j * lda] = ess;
+        Q[j + (long long)c1 * ldq] = ess;
+      }
+    }
+    if (pi != 0.0) {
+      const int jlo = max(bc0, k + 1);
+      for (int j = jlo + tid; j < bc1; j += blockDim.x)
+        sh_u[j - bc0] = (j == k + 1) ? 1.0 : a.rvec[j] / denr;
+      __syncthreads();
+      double acc[RPL];
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) acc[i] = 0.0;
+      // descending column order (snake against the A^T v pass)
+      const int nj = bc1 - jlo;
+      for (int jj = nj - 1 - warp; jj >= 0; jj -= kLabrdWarps) {
+        const int j = jlo + jj;
+        const double uj = sh_u[j - bc0];
+        const double* col = A + (long long)j * lda;
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) {
+          const int r = br0 + lane + 32 * i;
+          if (r < br1) acc[i] += col[r] * uj;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) sh_acc[warp * a.RB + lane + 32 * i] = acc[i];
+      __syncthreads();
+      for (int rr = tid; rr < a.RB; rr += blockDim.x) {
+        const int r = br0 + rr;
+        if (r < br1 && r > k) {
+          double s = 0.0;
+#pragma unroll
+          for (int w = 0; w < kLabrdWarps; ++w) s += sh_acc[w * a.RB + rr];
+          a.px[(long long)gc * a.ldpx + r] = s;
+        }
+      }
+      // Q^T u over this block's columns for t = gr, gr+Gr, ... < 2k+1
+      for (int t = gr + a.Gr * warp; t < c1; t += a.Gr * kLabrdWarps) {
+        const double* qc = Q + (long long)t * ldq;
+        double s = 0.0;
+        for (int j = jlo + lane; j < bc1; j += 32) s += qc[j] * sh_u[j - bc0];
+        s = warp_sum(s);
+        if (lane == 0) a.ps[gc * 64 + t] = s;
+      }
+    }
+    grid_barrier(a.bar, G, epoch);
+
+    // ================= phase 5: x, next column update
+    if (pi != 0.0 && tid < c1) {
+      double s = 0.0;
+      for (int q = 0; q < a.Gc; ++q) s += a.ps[q * 64 + tid];
+      sh_coef[tid] = s;
+    }
+    __syncthreads();
+    {
+      double part = 0.0;
+      const int r = r1lo + tid;
+      const bool next = k + 1 < nb;
+      if (tid < a.R1 && r < r1hi && r > k) {
+        double x = 0.0;
+        if (pi != 0.0) {
+          double s = 0.0;
+          for (int q = 0; q < a.Gc; ++q) s += a.px[(long long)q * a.ldpx + r];
+          double corr = 0.0;
+          for (int t = 0; t < c1; ++t) corr += P[r + (long long)t * ldp] * sh_coef[t];
+          x = pi * (s - corr);
+          P[r + (long long)c1 * ldp] = x;
+        }
+        if (next) {
+          // a[k+1:, k+1] -= P[k+1:, :2k+2] Q[k+1, :2k+2]   (Q[k+1,2k+1] = 1)
+          double upd = 0.0;
+          for (int t = 0; t < c1; ++t) upd += P[r + (long long)t * ldp] * Q[(k + 1) + (long long)t * ldq];
+          upd += x;
+          const double c = A[r + (long long)(k + 1) * lda] - upd;
+          A[r + (long long)(k + 1) * lda] = c;
+          a.cvec[r] = c;
+          if (r > k + 1) part = c * c;
+        }
+      }
+      if (next) {
+        part = block_sum(part, sh_red);
+        if (tid == 0) a.normc[g] = part;
+      }
+    }
+    if (k + 1 < nb) grid_barrier(a.bar, G, epoch);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Unblocked GEBD2 on a small trailing matrix (bidiag.py:75-110), one CTA.
+constexpr int kGebd2Threads = 1024;
+
+__global__ void __launch_bounds__(kGebd2Threads) gebd2_kernel(double* A, long long lda, int m, int n,
+                                                              double* d, double* e, double* tauq,
+                                                              double* taup, double* wbuf) {
+  __shared__ double sh_red[32];
+  __shared__ double sh_s[4];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  for (int k = 0; k < n; ++k) {
+    // column reflector
+    double part = 0.0;
+    for (int r = k + 1 + tid; r < m; r += blockDim.x) {
+      const double x = A[r + (long long)k * lda];
+      part += x * x;
+    }
+    const double nrm2 = block_sum(part, sh_red);
+    const double alpha = A[k + (long long)k * lda];
+    double tau, beta;
+    larfg_scalars(alpha, nrm2, tau, beta);
+    const double den = alpha - beta;
+    __syncthreads();
+    if (tid == 0) {
+      tauq[k] = tau;
+      d[k] = beta;
+      A[k + (long long)k * lda] = beta;
+    }
+    if (tau != 0.0)
+      for (int r = k + 1 + tid; r < m; r += blockDim.x) A[r + (long long)k * lda] /= den;
+    __syncthreads();
+    if (tau != 0.0 && k + 1 < n) {
+      // w_j = sum_{r>=k} v_r a[r,j]  (v_k = 1)
+      for (int j = k + 1 + warp; j < n; j += nw) {
+        const double* col = A + (long long)j * lda;
+        double s = 0.0;
+        for (int r = k + lane; r < m; r += 32) s += (r == k ? 1.0 : A[r + (long long)k * lda]) * col[r];
+        s = warp_sum(s);
+        if (lane == 0) wbuf[j] = s;
+      }
+      __syncthreads();
+      for (int j = k + 1; j < n; ++j) {
+        const double wj = wbuf[j];
+        for (int r = k + tid; r < m; r += blockDim.x) {
+          const double vr = r == k ? 1.0 : A[r + (long long)k * lda];
+          A[r + (long long)j * lda] -= tau * (vr * wj);
+        }
+      }
+      __syncthreads();
+    }
+    if (k < n - 1) {
+      // row reflector on a[k, k+1:]
+      part = 0.0;
+      for (int j = k + 2 + tid; j < n; j += blockDim.x) {
+        const double x = A[k + (long long)j * lda];
+        part += x * x;
+      }
+      const double nr2 = block_sum(part, sh_red);
+      const double al = A[k + (long long)(k + 1) * lda];
+      double pi, br;
+      larfg_scalars(al, nr2, pi, br);
+      const double dr = al - br;
+      __syncthreads();
+      if (tid == 0) {
+        taup[k] = pi;
+        e[k] = br;
+        A[k + (long long)(k + 1) * lda] = br;
+      }
+      if (pi != 0.0)
+        for (int j = k + 2 + tid; j < n; j += blockDim.x) A[k + (long long)j * lda] /= dr;
+      __syncthreads();
+      if (pi != 0.0) {
+        // w_r = sum_{j>=k+1} a[r,j] u_j for r >= k+1 (u_{k+1} = 1)
+        for (int r = k + 1 + tid; r < m; r += blockDim.x) {
+          double s = A[r + (long long)(k + 1) * lda];
+          for (int j = k + 2; j < n; ++j) s += A[r + (long long)j * lda] * A[k + (long long)j * lda];
+          wbuf[r] = s;
+        }
+        __syncthreads();
+        for (int j = k + 1; j < n; ++j) {
+          const double uj = j == k + 1 ? 1.0 : A[k + (long long)j * lda];
+          for (int r = k + 1 + tid; r < m; r += blockDim.x) A[r + (long long)j * lda] -= pi * (wbuf[r] * uj);
+        }
+        __syncthreads();
+      }
+    }
+    (void)sh_s;
+  }
+  if (tid == 0) taup[n - 1] = 0.0;
+}
+
+// ---------------------------------------------------------------------------
+template <int RPL>
+static int launch_labrd(cudaStream_t st, LabrdArgs& la, int grid, size_t smem) {
+  auto kern = labrd_kernel<RPL>;
+  static bool attr = false;
+  if (!attr) {
+    DC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  void* args[] = {&la};
+  DC_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(kLabrdThreads), args, smem, st));
+  note_launch();
+  return 0;
+}
+
+struct LabrdWork {
+  double *cvec, *rvec, *normc, *normr, *py, *px, *pw, *ps;
+  long long mp, np;
+};
+
+static size_t labrd_work_bytes(long long mp, long long np, int G) {
+  return pool_bytes(mp, 8) + pool_bytes(np, 8) + 2 * pool_bytes(G, 8) + pool_bytes((size_t)G * np, 8) +
+         pool_bytes((size_t)G * mp, 8) + 2 * pool_bytes((size_t)G * 64, 8);
+}
+
+static LabrdWork labrd_work_take(dcsvd_ctx* h, int pool, long long mp, long long np, int G) {
+  LabrdWork w;
+  w.cvec = pool_take<double>(h, pool, mp);
+  w.rvec = pool_take<double>(h, pool, np);
+  w.normc = pool_take<double>(h, pool, G);
+  w.normr = pool_take<double>(h, pool, G);
+  w.py = pool_take<double>(h, pool, (size_t)G * np);
+  w.px = pool_take<double>(h, pool, (size_t)G * mp);
+  w.pw = pool_take<double>(h, pool, (size_t)G * 64);
+  w.ps = pool_take<double>(h, pool, (size_t)G * 64);
+  w.mp = mp;
+  w.np = np;
+  return w;
+}
+
+// One LABRD panel on the mv x nv view Av (bidiag.py:113-165): P (mv x 2nb,
+// ldp) and Q (nv x 2nb, ldq) are zeroed here and filled; only the panel
+// rows/columns of Av change.
+static int labrd_launch(dcsvd_ctx* h, cudaStream_t st, int mv, int nv, double* Av, long long lda, int nb, double* d,
+                        double* e, double* tauq, double* taup, double* P, long long ldp, double* Q, long long ldq,
+                        const LabrdWork& w) {
+  const int G = h->sms;
+  DC_CUDA_TRY(cudaMemset2DAsync(P, sizeof(double) * ldp, 0, sizeof(double) * mv, 2 * nb, st));
+  DC_CUDA_TRY(cudaMemset2DAsync(Q, sizeof(double) * ldq, 0, sizeof(double) * nv, 2 * nb, st));
+  DC_CUDA_TRY(cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned), st));
+  // geometry: rows-per-lane by block aspect, Gr x Gc <= G
+  const double target_rows = mv / sqrt((double)G * mv / nv);
+  int rpl = 16;
+  if (target_rows <= 32 * 2) rpl = 2;
+  else if (target_rows <= 32 * 4) rpl = 4;
+  else if (target_rows <= 32 * 8) rpl = 8;
+  int RB = 32 * rpl;
+  int Gr = (mv + RB - 1) / RB;
+  if (Gr > G) return set_error(h, DCSVD_EINVAL, "matrix too tall for the GPU LABRD panel (%d rows)", mv);
+  int Gc = G / Gr;
+  if (Gc < 1) Gc = 1;
+  const int CB = (nv + Gc - 1) / Gc;
+  Gc = (nv + CB - 1) / CB;
+  const int grid = Gr * Gc;
+  LabrdArgs la;
+  la.A = Av; la.lda = lda; la.m = mv; la.n = nv; la.nb = nb;
+  la.P = P; la.Q = Q; la.ldp = ldp; la.ldq = ldq;
+  la.d = d; la.e = e; la.tauq = tauq; la.taup = taup;
+  la.cvec = w.cvec; la.rvec = w.rvec; la.normc = w.normc; la.normr = w.normr;
+  la.py = w.py; la.px = w.px; la.pw = w.pw; la.ps = w.ps; la.ldpy = w.np; la.ldpx = w.mp;
+  la.bar = h->d_bar;
+  la.Gr = Gr; la.Gc = Gc; la.RB = RB; la.CB = CB;
+  la.R1 = (mv + grid - 1) / grid;
+  la.C1 = (nv + grid - 1) / grid;
+  if (la.R1 > kLabrdThreads || la.C1 > kLabrdThreads)
+    return set_error(h, DCSVD_EINVAL, "matrix too large for one LABRD grid (%dx%d)", mv, nv);
+  const size_t smem = sizeof(double) * (((CB + 1) & ~1) + (size_t)kLabrdWarps * RB);
+  if (smem > 200 * 1024) return set_error(h, DCSVD_EINVAL, "LABRD block too wide (%d columns)", CB);
+  switch (rpl) {
+    case 2: return launch_labrd<2>(st, la, grid, smem);
+    case 4: return launch_labrd<4>(st, la, grid, smem);
+    case 8: return launch_labrd<8>(st, la, grid, smem);
+    default: return launch_labrd<16>(st, la, grid, smem);
+  }
+}
+
+int labrd_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A, long long lda, int nb, double* d,
+              double* e, double* tauq, double* taup, double* P, long long ldp, double* Q, long long ldq) {
+  if (!(1 <= nb && nb < n && n <= m))
+    return set_error(h, DCSVD_EINVAL, "panel width %d needs block < ncols <= nrows, view is %lldx%lld", nb, m, n);
+  if (nb > 32) return set_error(h, DCSVD_EINVAL, "GPU LABRD supports block width <= 32, got %d", nb);
+  int rc = pool_reserve(h, 0, labrd_work_bytes(m, n, h->sms), st);
+  if (rc) return rc;
+  LabrdWork w = labrd_work_take(h, 0, m, n, h->sms);
+  rc = labrd_launch(h, st, (int)m, (int)n, A, lda, nb, d, e, tauq, taup, P, ldp, Q, ldq, w);
+  if (rc) return rc;
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int gebrd_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A, long long lda,
+              double* d, double* e, double* tauq, double* taup, int nb) {
+  if (n < 1 || m < n) return set_error(h, DCSVD_EINVAL, "bidiagonalization requires m >= n >= 1, got %lldx%lld", m, n);
+  if (nb < 1) return set_error(h, DCSVD_EINVAL, "block width must be >= 1, got %d", nb);
+  if (nb > 32 && nb < n) return set_error(h, DCSVD_EINVAL, "GPU GEBRD supports block width <= 32, got %d", nb);
+  const bool unblocked = nb >= n;
+  if (unblocked) nb = (int)std::min<long long>(n, 32);  // no panel runs: the whole matrix goes through GEBD2
+  const int G = h->sms;
+  const long long mp = m, np = n;
+  size_t need = pool_bytes(mp * 2 * nb, 8) + pool_bytes(np * 2 * nb, 8) + labrd_work_bytes(mp, np, G) +
+                pool_bytes(mp + np, 8);
+  int rc = pool_reserve(h, 0, need, st);
+  if (rc) return rc;
+  double* P = pool_take<double>(h, 0, mp * 2 * nb);
+  double* Q = pool_take<double>(h, 0, np * 2 * nb);
+  LabrdWork w = labrd_work_take(h, 0, mp, np, G);
+  double* wbuf = pool_take<double>(h, 0, mp + np);
+  long long off = 0;
+  while (n - off > nb && !unblocked) {
+    const int mv = (int)(m - off), nv = (int)(n - off);
+    double* Av = A + off + off * lda;
+    rc = labrd_launch(h, st, mv, nv, Av, lda, nb, d + off, e + off, tauq + off, taup + off, P, mp, Q, np, w);
+    if (rc) return rc;
+    // trailing update A[nb:, nb:] -= P[nb:, :] Q[nb:, :]^T  (bidiag.py:195-197)
+    GemmDesc gd;
+    gd.m = mv - nb; gd.n = nv - nb; gd.k = 2 * nb;
+    gd.A = P + nb; gd.lda = mp; gd.acol = nullptr;
+    gd.B = Q + nb; gd.ldb = np;
+    gd.C = Av + nb + (long long)nb * lda; gd.ldc = lda; gd.ccol = nullptr;
+    gd.alpha = -1.0; gd.beta = 1.0;
+    rc = gemm_launch(st, false, true, gd);
+    if (rc) return rc;
+    off += nb;
+  }
+  gebd2_kernel<<<1, kGebd2Threads, 0, st>>>(A + off + off * lda, lda, (int)(m - off), (int)(n - off), d + off,
+                                            e + off, tauq + off, taup + off, wbuf);
+  note_launch();
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace dc

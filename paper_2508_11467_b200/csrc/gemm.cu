@@ -1,0 +1,257 @@
+// DMMA GEMM kernels (see gemm.cuh).
+#include "gemm.cuh"
+#include "launch.cuh"
+
+namespace dc {
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int bytes = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <bool TA, bool TB, int BM, int BN, int WARPS_M, int WARPS_N>
+struct GemmCfg {
+  static constexpr int BK = 16;
+  static constexpr int STAGES = 3;
+  static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
+  static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
+  static constexpr int FM = WTM / 8, FN = WTN / 8;
+  // A stage: TA ? [BM][BK+4] : [BK][BM+4];  B stage: TB ? [BK][BN+4] : [BN][BK+4]
+  static constexpr int LDA_S = TA ? (BK + 4) : (BM + 4);
+  static constexpr int LDB_S = TB ? (BN + 4) : (BK + 4);
+  static constexpr int A_ELEMS = TA ? BM * (BK + 4) : BK * (BM + 4);
+  static constexpr int B_ELEMS = TB ? BK * (BN + 4) : BN * (BK + 4);
+  static constexpr int SMEM_BYTES = STAGES * (A_ELEMS + B_ELEMS) * 8;
+};
+
+template <bool TA, bool TB, int BM, int BN, int WARPS_M, int WARPS_N>
+__global__ void __launch_bounds__(32 * WARPS_M * WARPS_N)
+    dgemm_kernel(GemmBatch batch, const GemmDesc* __restrict__ ddesc) {
+  using Cfg = GemmCfg<TA, TB, BM, BN, WARPS_M, WARPS_N>;
+  constexpr int BK = Cfg::BK, STAGES = Cfg::STAGES, THREADS = Cfg::THREADS;
+  const GemmDesc& P = ddesc ? ddesc[blockIdx.z] : batch.d[blockIdx.z];
+  const int M = P.m, N = P.n, K = P.k;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  if (m0 >= M || n0 >= N) return;
+
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + STAGES * Cfg::A_ELEMS;
+  const double* __restrict__ A = P.A;
+  const double* __restrict__ B = P.B;
+  const long long lda = P.lda, ldb = P.ldb;
+  const int* __restrict__ acol = P.acol;
+  const int tid = threadIdx.x;
+
+  auto load_tile = [&](int stage, int kt) {
+    const int k0 = kt * BK;
+    double* as = As + stage * Cfg::A_ELEMS;
+    double* bs = Bs + stage * Cfg::B_ELEMS;
+#pragma unroll
+    for (int e = tid; e < BM * BK; e += THREADS) {
+      int i, kk;
+      if (TA) { kk = e % BK; i = e / BK; } else { i = e % BM; kk = e / BM; }
+      const int gm = m0 + i, gk = k0 + kk;
+      const bool ok = gm < M && gk < K;
+      const double* src = A;
+      if (ok) {
+        if (TA) src = A + (long long)gk + (long long)gm * lda;
+        else {
+          const long long col = acol ? (long long)acol[gk] : (long long)gk;
+          src = A + (long long)gm + col * lda;
+        }
+      }
+      double* dst = TA ? as + i * Cfg::LDA_S + kk : as + kk * Cfg::LDA_S + i;
+      cp_async8(dst, src, ok);
+    }
+#pragma unroll
+    for (int e = tid; e < BN * BK; e += THREADS) {
+      int j, kk;
+      if (TB) { j = e % BN; kk = e / BN; } else { kk = e % BK; j = e / BK; }
+      const int gn = n0 + j, gk = k0 + kk;
+      const bool ok = gn < N && gk < K;
+      const double* src = B;
+      if (ok) src = TB ? B + (long long)gn + (long long)gk * ldb : B + (long long)gk + (long long)gn * ldb;
+      double* dst = TB ? bs + kk * Cfg::LDB_S + j : bs + j * Cfg::LDB_S + kk;
+      cp_async8(dst, src, ok);
+    }
+  };
+
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+  const int lr = lane >> 2, lc = lane & 3;
+  double acc[Cfg::FM][Cfg::FN][2];
+#pragma unroll
+  for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int KT = (K + BK - 1) / BK;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_tile(s, s);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    if (kt + STAGES - 1 < KT) load_tile((kt + STAGES - 1) % STAGES, kt + STAGES - 1);
+    cp_async_commit();
+    const double* as = As + (kt % STAGES) * Cfg::A_ELEMS;
+    const double* bs = Bs + (kt % STAGES) * Cfg::B_ELEMS;
+#pragma unroll
+    for (int ks = 0; ks < BK; ks += 4) {
+      double af[Cfg::FM], bf[Cfg::FN];
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i) {
+        const int m = wm * Cfg::WTM + i * 8 + lr;
+        af[i] = TA ? as[m * Cfg::LDA_S + ks + lc] : as[(ks + lc) * Cfg::LDA_S + m];
+      }
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j) {
+        const int n = wn * Cfg::WTN + j * 8 + lr;
+        bf[j] = TB ? bs[(ks + lc) * Cfg::LDB_S + n] : bs[n * Cfg::LDB_S + ks + lc];
+      }
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  double* __restrict__ C = P.C;
+  const long long ldc = P.ldc;
+  const double alpha = P.alpha, beta = P.beta;
+  const int* __restrict__ ccol = P.ccol;
+#pragma unroll
+  for (int j = 0; j < Cfg::FN; ++j) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int gn = n0 + wn * Cfg::WTN + j * 8 + lc * 2 + h;
+      if (gn >= N) continue;
+      const long long col = ccol ? (long long)ccol[gn] : (long long)gn;
+      double* cc = C + col * ldc;
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i) {
+        const int gm = m0 + wm * Cfg::WTM + i * 8 + lr;
+        if (gm < M) {
+          double v = alpha * acc[i][j][h];
+          if (beta != 0.0) v += beta * cc[gm];
+          cc[gm] = v;
+        }
+      }
+    }
+  }
+}
+
+template <bool TA, bool TB, int BM, int BN, int WM, int WN>
+static int launch_cfg(cudaStream_t st, const GemmBatch* b, const GemmDesc* dd, int nz, int max_m,
+                      int max_n) {
+  using Cfg = GemmCfg<TA, TB, BM, BN, WM, WN>;
+  auto kern = dgemm_kernel<TA, TB, BM, BN, WM, WN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    DC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+    attr_set = true;
+  }
+  dim3 grid((max_m + BM - 1) / BM, (max_n + BN - 1) / BN, nz);
+  GemmBatch empty;
+  empty.count = 0;
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(b ? *b : empty, dd);
+  note_launch();
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+template <bool TA, bool TB>
+static int launch_sized(cudaStream_t st, const GemmBatch* b, const GemmDesc* dd, int nz, int max_m,
+                        int max_n) {
+  // Big tiles when the output has enough of them to fill 148 SMs.
+  const long long tiles128 = (long long)((max_m + 127) / 128) * ((max_n + 127) / 128) * nz;
+  if (tiles128 >= 120) return launch_cfg<TA, TB, 128, 128, 4, 2>(st, b, dd, nz, max_m, max_n);
+  return launch_cfg<TA, TB, 64, 64, 2, 2>(st, b, dd, nz, max_m, max_n);
+}
+
+static int dispatch(cudaStream_t st, bool ta, bool tb, const GemmBatch* b, const GemmDesc* dd, int nz,
+                    int max_m, int max_n) {
+  if (max_m <= 0 || max_n <= 0 || nz <= 0) return 0;
+  if (!ta && !tb) return launch_sized<false, false>(st, b, dd, nz, max_m, max_n);
+  if (!ta && tb) return launch_sized<false, true>(st, b, dd, nz, max_m, max_n);
+  if (ta && !tb) return launch_sized<true, false>(st, b, dd, nz, max_m, max_n);
+  return launch_sized<true, true>(st, b, dd, nz, max_m, max_n);
+}
+
+int gemm_launch(cudaStream_t st, bool ta, bool tb, const GemmDesc& d) {
+  if (d.m <= 0 || d.n <= 0) return 0;
+  GemmBatch b;
+  b.d[0] = d;
+  b.count = 1;
+  return dispatch(st, ta, tb, &b, nullptr, 1, d.m, d.n);
+}
+
+int gemm_launch_batch(cudaStream_t st, bool ta, bool tb, const GemmBatch& b) {
+  int mm = 0, nn = 0;
+  for (int i = 0; i < b.count; ++i) {
+    mm = b.d[i].m > mm ? b.d[i].m : mm;
+    nn = b.d[i].n > nn ? b.d[i].n : nn;
+  }
+  return dispatch(st, ta, tb, &b, nullptr, b.count, mm, nn);
+}
+
+int gemm_launch_device(cudaStream_t st, bool ta, bool tb, const GemmDesc* ddesc, int ndesc, int max_m,
+                       int max_n) {
+  return dispatch(st, ta, tb, nullptr, ddesc, ndesc, max_m, max_n);
+}
+
+// ---------------------------------------------------------------------------
+// GEMV (densecore.matvec_accumulate); not on the SVD hot path, exported for
+// API completeness.  y <- alpha op(A) x + beta y.
+__global__ void dgemv_t_kernel(int m, int n, double alpha, const double* __restrict__ A, long long lda,
+                               const double* __restrict__ x, double beta, double* __restrict__ y) {
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= n) return;
+  double s = 0.0;
+  const double* a = A + (long long)j * lda;
+  for (int i = lane; i < m; i += 32) s += a[i] * x[i];
+  s = warp_sum(s);
+  if (lane == 0) y[j] = alpha * s + (beta != 0.0 ? beta * y[j] : 0.0);
+}
+__global__ void dgemv_n_kernel(int m, int n, double alpha, const double* __restrict__ A, long long lda,
+                               const double* __restrict__ x, double beta, double* __restrict__ y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double s = 0.0;
+  for (int j = 0; j < n; ++j) s += A[i + (long long)j * lda] * x[j];
+  y[i] = alpha * s + (beta != 0.0 ? beta * y[i] : 0.0);
+}
+
+int gemv_launch(cudaStream_t st, bool ta, int m, int n, double alpha, const double* A, long long lda,
+                const double* x, double beta, double* y) {
+  if (ta) {
+    if (n <= 0) return 0;
+    dgemv_t_kernel<<<(n + 7) / 8, 256, 0, st>>>(m, n, alpha, A, lda, x, beta, y);
+  } else {
+    if (m <= 0) return 0;
+    dgemv_n_kernel<<<(m + 255) / 256, 256, 0, st>>>(m, n, alpha, A, lda, x, beta, y);
+  }
+  note_launch();
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace dc

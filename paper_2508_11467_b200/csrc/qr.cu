@@ -1,0 +1,446 @@
+// Householder QR (GEQRF/ORGQR) and the bidiagonal back-transformations
+// (ORMBR) with inverse-T compact-WY block reflectors.
+//
+// Reference: pkg/src/dcsvd/qrblock.py (geqrf_panel :51-71, _panel_y :74-87,
+// build_tinv :90-100, apply_block_reflector_left/right :103-119, geqrf_blocked
+// :122-144, orgqr :147-164) and pkg/src/dcsvd/backtransform.py:60-131;
+// arxiv 2508.11467 modified CWY.
+//
+// Every block application is DMMA GEMM work: Z = Y^T C (split-K over the long
+// dimension with a fixed-order partial reduction), G = Y^T Y in the same
+// batched launch, one CTA turns G into T^-1 = triu(G,1) + diag(1/tau) and
+// inverts it (so the reference's TRSM becomes one small GEMM X = T Z), then
+// C -= Y X.  The unblocked QR panel is a cooperative kernel that keeps each
+// CTA's row slab of the panel in shared memory for all its columns.
+#include "ctx.cuh"
+#include "gemm.cuh"
+#include "launch.cuh"
+
+namespace dc {
+
+// ---------------------------------------------------------------------------
+// Y / Y^T construction from packed reflector storage.
+//  ymode 0 ('Q' / QR): Y (rows x w, ld rows) from src = packed + off + off*lda:
+//     Y[r,t] = r == t ? 1 : r > t ? src[r + t*lda] : 0, zero column if tau[t] == 0
+//  ymode 1 ('P'): Yt (w x rows, ld w) from src = packed + off + (off+1)*lda:
+//     Yt[t,r] = r == t ? 1 : r > t ? src[t + r*lda] : 0, zero row if tau[t] == 0
+__global__ void build_y_kernel(int ymode, const double* __restrict__ src, long long lda,
+                               const double* __restrict__ tau, int rows, int w, double* __restrict__ Y) {
+  const long long total = (long long)rows * w;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int r, t;
+    if (ymode == 0) { r = (int)(idx % rows); t = (int)(idx / rows); }
+    else { t = (int)(idx % w); r = (int)(idx / w); }
+    double v = 0.0;
+    if (tau[t] != 0.0) {
+      if (r == t) v = 1.0;
+      else if (r > t) v = ymode == 0 ? src[r + (long long)t * lda] : src[t + (long long)r * lda];
+    }
+    Y[idx] = v;
+  }
+}
+
+// G = sum_s Gp[s]; Tinv = triu(G,1) + diag(1/tau) (1 when tau == 0);
+// T = Tinv^-1 (upper); Top = trans ? T^T : T  (w x w, ld w).
+__global__ void cwy_finish_kernel(const double* __restrict__ Gp, int S, int w, const double* __restrict__ tau,
+                                  int trans, double* __restrict__ Top, int* err) {
+  __shared__ double ti[64 * 65];
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < w * w; idx += blockDim.x) {
+    const int i = idx % w, j = idx / w;
+    double v = 0.0;
+    if (i < j) {
+      for (int s = 0; s < S; ++s) v += Gp[(long long)s * w * w + idx];
+    } else if (i == j) {
+      v = tau[i] != 0.0 ? 1.0 / tau[i] : 1.0;
+    }
+    ti[i + j * 65] = v;
+  }
+  __syncthreads();
+  if (tid < w) {
+    if (ti[tid + tid * 65] == 0.0) raise_dev(err, kDevSingularT);
+    // column j = tid of T = Tinv^-1 by back substitution (thread-private column)
+    const int j = tid;
+    double* tcol = Top + (long long)j * w;
+    for (int i = w - 1; i >= 0; --i) {
+      double v = 0.0;
+      if (i <= j) {
+        double s = (i == j) ? 1.0 : 0.0;
+        for (int l = i + 1; l <= j; ++l) s -= ti[i + l * 65] * tcol[l];
+        v = s / ti[i + i * 65];
+      }
+      tcol[i] = v;
+    }
+  }
+  if (!trans) return;
+  __syncthreads();
+  for (int idx = tid; idx < w * w; idx += blockDim.x) ti[(idx % w) + (idx / w) * 65] = Top[idx];
+  __syncthreads();
+  for (int idx = tid; idx < w * w; idx += blockDim.x) {
+    const int i = idx % w, j = idx / w;
+    Top[idx] = ti[j + i * 65];
+  }
+}
+
+__global__ void splitk_reduce_kernel(double* __restrict__ Zp, long long count, int S) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    double v = Zp[i];
+    for (int s = 1; s < S; ++s) v += Zp[(long long)s * count + i];
+    Zp[i] = v;
+  }
+}
+
+static int grid_for(long long n, int threads = 256) {
+  long long g = (n + threads - 1) / threads;
+  if (g > 148 * 16) g = 148 * 16;
+  return (int)(g < 1 ? 1 : g);
+}
+
+// Apply the block reflector with Y (ytrans == false: Y rows_y x w, ld rows_y;
+// ytrans == true: Yt w x rows_y, ld w) to C.  side 'L': C (rows_y x ncols)
+// <- (I - Y op(T) Y^T) C.  side 'R': C (nrows x rows_y) <- C (I - Y op(T) Y^T).
+// op(T) = T or T^T (trans).  Scratch from pool 0 at `scratch` (caller sized
+// via cwy_scratch_doubles).
+static size_t cwy_scratch_doubles(long long rows_y, long long c_other, int w) {
+  const int S = 4;
+  return (size_t)S * (size_t)w * (size_t)c_other + (size_t)S * w * w + (size_t)w * w + 64;
+}
+
+static int cwy_apply(dcsvd_ctx* h, cudaStream_t st, char side, bool trans, bool ytrans, const double* Y,
+                     long long ldy, const double* tau, int w, long long rows_y, double* C, long long ldc,
+                     long long c_other, double* scratch) {
+  if (rows_y <= 0 || c_other <= 0 || w <= 0) return 0;
+  // split-K so that Z's tiles x S fill the GPU
+  const long long zt = (c_other + 63) / 64;
+  int S = 1;
+  while (S < 4 && zt * S < 2 * h->sms && rows_y / (S * 2) >= 256) S *= 2;
+  double* Zp = scratch;
+  double* Gp = Zp + (size_t)S * w * c_other;
+  double* Top = Gp + (size_t)S * w * w;
+  const long long kchunk = (rows_y + S - 1) / S;
+  GemmBatch zb, gb;
+  zb.count = 0;
+  gb.count = 0;
+  for (int s = 0; s < S; ++s) {
+    const long long k0 = s * kchunk;
+    const long long kk = std::min(kchunk, rows_y - k0);
+    GemmDesc z, g;
+    z.acol = nullptr; z.ccol = nullptr; z.alpha = 1.0; z.beta = 0.0;
+    g = z;
+    // op(Y^T) rows k0.. : Y stored normal -> A = Y + k0 (transA); Yt -> A = Yt + k0*ldy
+    const double* Yk = ytrans ? Y + k0 * ldy : Y + k0;
+    if (side == 'L') {
+      z.m = w; z.n = (int)c_other; z.k = (int)kk;
+      z.A = Yk; z.lda = ldy;
+      z.B = C + k0; z.ldb = ldc;
+      z.C = Zp + (size_t)s * w * c_other; z.ldc = w;
+    } else {
+      z.m = (int)c_other; z.n = w; z.k = (int)kk;
+      z.A = C + k0 * ldc; z.lda = ldc;
+      z.B = Yk; z.ldb = ldy;
+      z.C = Zp + (size_t)s * w * c_other; z.ldc = c_other;
+    }
+    g.m = w; g.n = w; g.k = (int)kk;
+    g.A = Yk; g.lda = ldy; g.B = Yk; g.ldb = ldy;
+    g.C = Gp + (size_t)s * w * w; g.ldc = w;
+    zb.d[zb.count++] = z;
+    gb.d[gb.count++] = g;
+  }
+  int rc;
+  if (side == 'L') rc = gemm_launch_batch(st, /*ta=*/!ytrans, /*tb=*/false, zb);
+  else rc = gemm_launch_batch(st, false, /*tb=*/ytrans, zb);
+  if (rc) return rc;
+  rc = gemm_launch_batch(st, !ytrans, ytrans, gb);
+  if (rc) return rc;
+  cwy_finish_kernel<<<1, 256, 0, st>>>(Gp, S, w, tau, trans ? 1 : 0, Top, h->d_err);
+  note_launch();
+  const long long zc = (long long)w * c_other;
+  if (S > 1) {
+    splitk_reduce_kernel<<<grid_for(zc), 256, 0, st>>>(Zp, zc, S);
+    note_launch();
+  }
+  // X = op(T) Z  (left, w x c_other) or Z op(T) (right, c_other x w); in place
+  // is not possible, so write X into the second partial slot (or a tail slot).
+  double* X = (S > 1) ? Zp + zc : Gp;  // Gp is free after finish when S == 1? no: keep separate
+  if (S == 1) X = Top + (size_t)w * w;  // scratch tail sized below
+  GemmDesc xd;
+  xd.acol = nullptr; xd.ccol = nullptr; xd.alpha = 1.0; xd.beta = 0.0;
+  if (side == 'L') {
+    xd.m = w; xd.n = (int)c_other; xd.k = w;
+    xd.A = Top; xd.lda = w; xd.B = Zp; xd.ldb = w; xd.C = X; xd.ldc = w;
+  } else {
+    xd.m = (int)c_other; xd.n = w; xd.k = w;
+    xd.A = Zp; xd.lda = c_other; xd.B = Top; xd.ldb = w; xd.C = X; xd.ldc = c_other;
+  }
+  rc = gemm_launch(st, false, false, xd);
+  if (rc) return rc;
+  GemmDesc ud;
+  ud.acol = nullptr; ud.ccol = nullptr; ud.alpha = -1.0; ud.beta = 1.0;
+  if (side == 'L') {
+    // C -= Y X : op(A) = Y
+    ud.m = (int)rows_y; ud.n = (int)c_other; ud.k = w;
+    ud.A = Y; ud.lda = ldy; ud.B = X; ud.ldb = w; ud.C = C; ud.ldc = ldc;
+    return gemm_launch(st, /*ta=*/ytrans, false, ud);
+  }
+  // C -= X Y^T : op(B) = Y^T
+  ud.m = (int)c_other; ud.n = (int)rows_y; ud.k = w;
+  ud.A = X; ud.lda = c_other; ud.B = Y; ud.ldb = ldy; ud.C = C; ud.ldc = ldc;
+  return gemm_launch(st, false, /*tb=*/!ytrans, ud);
+}
+
+static size_t cwy_total_scratch(long long rows_y, long long c_other, int w) {
+  // partials (S<=4) + G partials + Top + X (when S == 1)
+  return cwy_scratch_doubles(rows_y, c_other, w) + (size_t)w * c_other + 64;
+}
+
+// ---------------------------------------------------------------------------
+// GEQR2 panel (qrblock.py:51-71): cooperative, each CTA keeps its row slab of
+// the m x w panel in shared memory (ld = slab rows).
+struct Geqr2Args {
+  double* A;
+  long long lda;
+  int m, w;
+  double* tau;
+  double* part;  // G x 64 partials
+  unsigned* bar;
+  int R1;        // rows per CTA
+};
+
+constexpr int kGeqr2Threads = 256;
+
+__global__ void __launch_bounds__(kGeqr2Threads, 1) geqr2_coop_kernel(Geqr2Args a) {
+  extern __shared__ double slab[];  // R1 x w
+  __shared__ double sh_red[32];
+  __shared__ double sh_w[64];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int g = blockIdx.x, G = gridDim.x;
+  const int r0 = g * a.R1, r1 = min(a.m, r0 + a.R1), nr = max(0, r1 - r0);
+  const int R1 = a.R1, w = a.w;
+  unsigned epoch = 0;
+  for (int idx = tid; idx < nr * w; idx += blockDim.x) {
+    const int rr = idx % nr, t = idx / nr;
+    slab[rr + t * R1] = a.A[(r0 + rr) + (long long)t * a.lda];
+  }
+  __syncthreads();
+  // norm partial of column 0 (rows > 0)
+  {
+    double p = 0.0;
+    for (int rr = tid; rr < nr; rr += blockDim.x)
+      if (r0 + rr > 0) p += slab[rr] * slab[rr];
+    p = block_sum(p, sh_red);
+    if (tid == 0) a.part[g * 64 + 0] = p;
+  }
+  grid_barrier(a.bar, G, epoch);
+  for (int j = 0; j < w; ++j) {
+    // ---- LARFG of column j
+    double p = 0.0;
+    for (int i = tid; i < G; i += blockDim.x) p += a.part[i * 64 + 0];
+    const double nrm2 = block_sum(p, sh_red);
+    // alpha = a[j,j]: the row owner publishes it to global A before the barrier
+    const double alpha = a.A[j + (long long)j * a.lda];
+    double tau, beta;
+    {
+      const double xn = sqrt(nrm2);
+      if (xn == 0.0) { tau = 0.0; beta = alpha; }
+      else { beta = -copysign(hypot(alpha, xn), alpha); tau = (beta - alpha) / beta; }
+    }
+    const double den = alpha - beta;
+    if (g == 0 && tid == 0) a.tau[j] = tau;
+    for (int rr = tid; rr < nr; rr += blockDim.x) {
+      const int r = r0 + rr;
+      if (r == j) slab[rr + j * R1] = beta;
+      else if (r > j && tau != 0.0) slab[rr + j * R1] /= den;
+    }
+    __syncthreads();
+    // partial w_t = sum_{r>=j} v_r a[r,t], t in (j, w)
+    if (tau != 0.0 && j + 1 < w) {
+      for (int t = j + 1 + warp; t < w; t += nw) {
+        double s = 0.0;
+        for (int rr = lane; rr < nr; rr += 32) {
+          const int r = r0 + rr;
+          if (r >= j) s += (r == j ? 1.0 : slab[rr + j * R1]) * slab[rr + t * R1];
+        }
+        s = warp_sum(s);
+        if (lane == 0) a.part[g * 64 + t] = s;
+      }
+    }
+    grid_barrier(a.bar, G, epoch);
+    if (tau != 0.0 && j + 1 < w) {
+      if (tid < w && tid > j) {
+        double s = 0.0;
+        for (int i = 0; i < G; ++i) s += a.part[i * 64 + tid];
+        sh_w[tid] = s;
+      }
+      __syncthreads();
+      for (int idx = tid; idx < nr * (w - j - 1); idx += blockDim.x) {
+        const int rr = idx % nr, t = j + 1 + idx / nr;
+        const int r = r0 + rr;
+        if (r >= j) {
+          const double v = r == j ? 1.0 : slab[rr + j * R1];
+          slab[rr + t * R1] -= tau * (v * sh_w[t]);
+        }
+      }
+      __syncthreads();
+    }
+    if (j + 1 < w) {
+      // publish a[j+1, j+1] (alpha of the next column) and the norm partial
+      double q = 0.0;
+      for (int rr = tid; rr < nr; rr += blockDim.x) {
+        const int r = r0 + rr;
+        const double x = slab[rr + (j + 1) * R1];
+        if (r > j + 1) q += x * x;
+        if (r == j + 1) a.A[r + (long long)(j + 1) * a.lda] = x;
+      }
+      q = block_sum(q, sh_red);
+      // slot 0 was consumed by every CTA before the previous barrier
+      if (tid == 0) a.part[g * 64 + 0] = q;
+      grid_barrier(a.bar, G, epoch);
+    }
+  }
+  for (int idx = tid; idx < nr * w; idx += blockDim.x) {
+    const int rr = idx % nr, t = idx / nr;
+    a.A[(r0 + rr) + (long long)t * a.lda] = slab[rr + t * R1];
+  }
+}
+
+static int geqr2_launch(dcsvd_ctx* h, cudaStream_t st, double* A, long long lda, int m, int w, double* tau,
+                        double* part) {
+  int G = h->sms;
+  int R1 = (m + G - 1) / G;
+  if (R1 < 32) {
+    R1 = 32;
+    G = (m + R1 - 1) / R1;
+  }
+  const size_t smem = sizeof(double) * (size_t)R1 * w;
+  if (smem > 200 * 1024) return set_error(h, DCSVD_EINVAL, "QR panel too tall for the GPU panel kernel (%d x %d)", m, w);
+  static bool attr = false;
+  if (!attr) {
+    DC_CUDA_TRY(cudaFuncSetAttribute(geqr2_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  DC_CUDA_TRY(cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned), st));
+  Geqr2Args a;
+  a.A = A; a.lda = lda; a.m = m; a.w = w; a.tau = tau; a.part = part; a.bar = h->d_bar; a.R1 = R1;
+  void* args[] = {&a};
+  DC_CUDA_TRY(cudaLaunchCooperativeKernel((void*)geqr2_coop_kernel, dim3(G), dim3(kGeqr2Threads), args, smem, st));
+  note_launch();
+  return 0;
+}
+
+int geqrf_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A, long long lda, double* tau,
+              int nb) {
+  if (n < 1) return set_error(h, DCSVD_EINVAL, "matrix must have at least one column");
+  if (m < n) return set_error(h, DCSVD_EINVAL, "QR factorization requires m >= n, got %lldx%lld", m, n);
+  if (nb < 1) return set_error(h, DCSVD_EINVAL, "block width must be >= 1, got %d", nb);
+  if (nb > 64) return set_error(h, DCSVD_EINVAL, "GPU QR supports block width <= 64, got %d", nb);
+  const size_t need = pool_bytes((size_t)m * nb, 8) + pool_bytes((size_t)h->sms * 64 + 64, 8) +
+                      pool_bytes(cwy_total_scratch(m, n, nb), 8);
+  int rc = pool_reserve(h, 0, need, st);
+  if (rc) return rc;
+  double* Y = pool_take<double>(h, 0, (size_t)m * nb);
+  double* part = pool_take<double>(h, 0, (size_t)h->sms * 64 + 64);
+  double* scr = pool_take<double>(h, 0, cwy_total_scratch(m, n, nb));
+  for (long long off = 0; off < n; off += nb) {
+    const int w = (int)std::min<long long>(nb, n - off);
+    const long long rows = m - off;
+    rc = geqr2_launch(h, st, A + off + off * lda, lda, (int)rows, w, tau + off, part);
+    if (rc) return rc;
+    if (off + w < n) {
+      build_y_kernel<<<grid_for(rows * w), 256, 0, st>>>(0, A + off + off * lda, lda, tau + off, (int)rows, w, Y);
+      note_launch();
+      rc = cwy_apply(h, st, 'L', /*trans=*/true, false, Y, rows, tau + off, w, rows, A + off + (off + w) * lda, lda,
+                     n - off - w, scr);
+      if (rc) return rc;
+    }
+  }
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+__global__ void eye_kernel(double* Q, long long ldq, long long m, long long k) {
+  const long long total = m * k;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long i = idx % m, j = idx / m;
+    Q[i + j * ldq] = (i == j) ? 1.0 : 0.0;
+  }
+}
+
+int orgqr_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long nrefl, long long k, const double* A,
+              long long lda, const double* tau, double* Q, long long ldq, int nb) {
+  if (k < 1 || k > m) return set_error(h, DCSVD_EINVAL, "need 1 <= k <= %lld columns of Q, got %lld", m, k);
+  if (nb < 1 || nb > 64) return set_error(h, DCSVD_EINVAL, "GPU ORGQR supports block width 1..64, got %d", nb);
+  const size_t need = pool_bytes((size_t)m * nb, 8) + pool_bytes(cwy_total_scratch(m, k, nb), 8);
+  int rc = pool_reserve(h, 0, need, st);
+  if (rc) return rc;
+  double* Y = pool_take<double>(h, 0, (size_t)m * nb);
+  double* scr = pool_take<double>(h, 0, cwy_total_scratch(m, k, nb));
+  eye_kernel<<<grid_for(m * k), 256, 0, st>>>(Q, ldq, m, k);
+  note_launch();
+  long long last = ((nrefl - 1) / nb) * nb;
+  for (long long off = last; off >= 0; off -= nb) {
+    const int w = (int)std::min<long long>(nb, nrefl - off);
+    const long long rows = m - off;
+    if (off >= k) continue;  // columns >= off are all that change; none exist
+    build_y_kernel<<<grid_for(rows * w), 256, 0, st>>>(0, A + off + off * lda, lda, tau + off, (int)rows, w, Y);
+    note_launch();
+    // columns < off of Q stay exactly e_i (zero in rows >= off)
+    rc = cwy_apply(h, st, 'L', false, false, Y, rows, tau + off, w, rows, Q + off + off * ldq, ldq, k - off, scr);
+    if (rc) return rc;
+  }
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int ormbr_run(dcsvd_ctx* h, cudaStream_t st, char vect, bool trans, long long m, long long n, const double* A,
+              long long lda, const double* tau, double* C, long long c_rows, long long c_cols, long long ldc,
+              int nb) {
+  if (nb < 1 || nb > 64) return set_error(h, DCSVD_EINVAL, "GPU ORMBR supports block width 1..64, got %d", nb);
+  if (vect == 'Q') {
+    if (c_rows != m) return set_error(h, DCSVD_EINVAL, "C has %lld rows, sequence acts on %lld", c_rows, m);
+    const long long count = n;
+    const size_t need = pool_bytes((size_t)m * nb, 8) + pool_bytes(cwy_total_scratch(m, c_cols, nb), 8);
+    int rc = pool_reserve(h, 0, need, st);
+    if (rc) return rc;
+    double* Y = pool_take<double>(h, 0, (size_t)m * nb);
+    double* scr = pool_take<double>(h, 0, cwy_total_scratch(m, c_cols, nb));
+    const long long nblk = (count + nb - 1) / nb;
+    for (long long b = 0; b < nblk; ++b) {
+      const long long bi = trans ? b : nblk - 1 - b;  // U1^T front-to-back, U1 back-to-front
+      const long long off = bi * nb;
+      const int w = (int)std::min<long long>(nb, count - off);
+      const long long rows = m - off;
+      build_y_kernel<<<grid_for(rows * w), 256, 0, st>>>(0, A + off + off * lda, lda, tau + off, (int)rows, w, Y);
+      note_launch();
+      rc = cwy_apply(h, st, 'L', trans, false, Y, rows, tau + off, w, rows, C + off, ldc, c_cols, scr);
+      if (rc) return rc;
+    }
+  } else if (vect == 'P') {
+    if (c_cols != n) return set_error(h, DCSVD_EINVAL, "C has %lld columns, sequence acts on %lld", c_cols, n);
+    const long long count = n > 0 ? n - 1 : 0;
+    const size_t need = pool_bytes((size_t)n * nb, 8) + pool_bytes(cwy_total_scratch(n, c_rows, nb), 8);
+    int rc = pool_reserve(h, 0, need, st);
+    if (rc) return rc;
+    double* Yt = pool_take<double>(h, 0, (size_t)n * nb);
+    double* scr = pool_take<double>(h, 0, cwy_total_scratch(n, c_rows, nb));
+    const long long nblk = (count + nb - 1) / nb;
+    for (long long b = 0; b < nblk; ++b) {
+      const long long bi = trans ? nblk - 1 - b : b;  // V1^T back-to-front, V1 front-to-back
+      const long long off = bi * nb;
+      const int w = (int)std::min<long long>(nb, count - off);
+      const long long rows = n - off - 1;
+      build_y_kernel<<<grid_for(rows * w), 256, 0, st>>>(1, A + off + (off + 1) * lda, lda, tau + off, (int)rows, w, Yt);
+      note_launch();
+      rc = cwy_apply(h, st, 'R', trans, true, Yt, w, tau + off, w, rows, C + (off + 1) * ldc, ldc, c_rows, scr);
+      if (rc) return rc;
+    }
+  } else {
+    return set_error(h, DCSVD_EINVAL, "vect must be 'Q' or 'P'");
+  }
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace dc
