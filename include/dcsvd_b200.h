@@ -61,6 +61,13 @@ int dcsvd_version(void);
 /* Number of this library's kernels launched through `h` since creation. */
 long long dcsvd_launch_count(dcsvd_handle h);
 
+/* Kernel-family timing for roofline reporting.  When enabled, CUDA events
+ * bracket every launch of a family on its stream.  kind 0 = LABRD panel kernel
+ * (work = algorithmic GEMV bytes), kind 1 = DMMA GEMM (work = flops).
+ * dcsvd_set_stats also clears previous records; dcsvd_get_stats synchronizes. */
+int dcsvd_set_stats(dcsvd_handle h, int enable);
+int dcsvd_get_stats(dcsvd_handle h, int kind, double* ms, double* work, long long* launches);
+
 /* GEMM: C <- alpha*op(A)*op(B) + beta*C (beta == 0 does not read C).
  * Replaces densecore.matmul_accumulate (pkg/src/dcsvd/densecore.py:73-93).
  * Hand-written DMMA (mma.sync m8n8k4 f64) kernel. */

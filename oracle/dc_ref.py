@@ -92,9 +92,9 @@ def _small(x, a, b, bnorm):
 def _shift(d, e, lo, hi):
     # Wilkinson shift of the trailing 2x2 of B^T B (bdc.py:205-215)
     ep = e[hi - 2] if hi - 2 >= lo else 0.0
-    a11 = d[hi - 1] ** 2 + ep * ep
+    a11 = d[hi - 1] * d[hi - 1] + ep * ep
     a12 = d[hi - 1] * e[hi - 1]
-    a22 = d[hi] ** 2 + e[hi - 1] ** 2
+    a22 = d[hi] * d[hi] + e[hi - 1] * e[hi - 1]
     h = 0.5 * (a11 - a22)
     den = h + np.copysign(np.hypot(h, a12), h if h != 0.0 else 1.0)
     return a22 if den == 0.0 else a22 - a12 * a12 / den

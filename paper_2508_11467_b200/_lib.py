@@ -21,7 +21,7 @@ OK, EINVAL, ENOCONV, EARITH, ESINGULAR, ECUDA = range(6)
 EXPORTED = (
     "dcsvd_create", "dcsvd_destroy", "dcsvd_last_error", "dcsvd_version", "dcsvd_launch_count",
     "dcsvd_dgemm", "dcsvd_dgemv", "dcsvd_gebrd", "dcsvd_labrd", "dcsvd_bdsdc", "dcsvd_geqrf",
-    "dcsvd_orgqr", "dcsvd_ormbr", "dcsvd_gesdd", "dcsvd_gesdd_batched",
+    "dcsvd_orgqr", "dcsvd_ormbr", "dcsvd_gesdd", "dcsvd_gesdd_batched", "dcsvd_set_stats", "dcsvd_get_stats",
 )
 
 
@@ -71,6 +71,8 @@ def load_library(path=None):
             "dcsvd_last_error": (ctypes.c_char_p, [V]),
             "dcsvd_version": (I, []),
             "dcsvd_launch_count": (ctypes.c_longlong, [V]),
+            "dcsvd_set_stats": (I, [V, I]),
+            "dcsvd_get_stats": (I, [V, I, ctypes.POINTER(D), ctypes.POINTER(D), ctypes.POINTER(ctypes.c_longlong)]),
             "dcsvd_dgemm": (I, [V, I, I, I64, I64, I64, D, V, I64, V, I64, D, V, I64, V]),
             "dcsvd_dgemv": (I, [V, I, I64, I64, D, V, I64, V, D, V, V]),
             "dcsvd_gebrd": (I, [V, I64, I64, V, I64, V, V, V, V, I, V]),
@@ -207,3 +209,16 @@ def ptr(t):
 def ld(t):
     """Leading dimension of a column-major 2-d tensor."""
     return max(int(t.stride(1)), max(int(t.shape[0]), 1)) if t.shape[1] > 1 else max(int(t.shape[0]), 1)
+
+
+def set_stats(enable, device=None):
+    h = handle(device)
+    check(load_library().dcsvd_set_stats(h, int(bool(enable))), h)
+
+
+def get_stats(kind, device=None):
+    """(milliseconds, work, launches) accumulated for a kernel family."""
+    h = handle(device)
+    ms, work, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_longlong()
+    check(load_library().dcsvd_get_stats(h, int(kind), ctypes.byref(ms), ctypes.byref(work), ctypes.byref(n)), h)
+    return ms.value, work.value, n.value

@@ -48,6 +48,22 @@ int pool_reserve(dcsvd_ctx* h, int p, size_t bytes, cudaStream_t st) {
   return 0;
 }
 
+int stat_begin(dcsvd_ctx* h, int kind, double work, cudaStream_t st) {
+  if (!h || !h->stats_on) return -1;
+  dcsvd_ctx::StatRec r;
+  r.kind = kind;
+  r.work = work;
+  cudaEventCreate(&r.a);
+  cudaEventCreate(&r.b);
+  cudaEventRecord(r.a, st);
+  h->stats.push_back(r);
+  return (int)h->stats.size() - 1;
+}
+void stat_end(dcsvd_ctx* h, int idx, cudaStream_t st) {
+  if (idx < 0) return;
+  cudaEventRecord(h->stats[idx].b, st);
+}
+
 int check_device_status(dcsvd_ctx* h, cudaStream_t st, const char* stage) {
   cudaError_t e = cudaMemcpyAsync(h->h_err, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -299,6 +315,38 @@ int dcsvd_destroy(dcsvd_handle h) {
   cudaFree(h->d_bar);
   cudaFreeHost(h->h_err);
   delete h;
+  return 0;
+}
+
+int dcsvd_set_stats(dcsvd_handle h, int enable) {
+  if (!h) return DCSVD_EINVAL;
+  cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  for (auto& r : h->stats) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  h->stats.clear();
+  h->stats_on = enable != 0;
+  return 0;
+}
+
+int dcsvd_get_stats(dcsvd_handle h, int kind, double* ms, double* work, long long* launches) {
+  if (!h) return DCSVD_EINVAL;
+  cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  double t = 0.0, w = 0.0;
+  long long c = 0;
+  for (auto& r : h->stats) {
+    if (r.kind != kind) continue;
+    float x = 0.f;
+    if (cudaEventElapsedTime(&x, r.a, r.b) == cudaSuccess) t += x;
+    w += r.work;
+    ++c;
+  }
+  if (ms) *ms = t;
+  if (work) *work = w;
+  if (launches) *launches = c;
   return 0;
 }
 

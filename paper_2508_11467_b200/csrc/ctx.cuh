@@ -20,6 +20,15 @@ struct dcsvd_ctx {
   unsigned* d_bar = nullptr;    // grid-barrier counters (kNumBars)
   int* h_err = nullptr;         // pinned mirror of d_err
   DevPool pool[3];              // 0: stage scratch, 1: driver buffers, 2: bdc
+  // optional per-kernel-family timing (bench roofline): CUDA events around
+  // each launch of a family, with its algorithmic bytes/flops
+  bool stats_on = false;
+  struct StatRec {
+    int kind;
+    cudaEvent_t a, b;
+    double work;
+  };
+  std::vector<StatRec> stats;
 };
 
 namespace dc {
@@ -41,6 +50,9 @@ inline T* pool_take(dcsvd_ctx* h, int p, size_t count) {
 inline size_t pool_bytes(size_t count, size_t elem) { return (count * elem + 255) & ~size_t(255); }
 
 int set_error(dcsvd_ctx* h, int code, const char* fmt, ...);
+// stats helpers: stat_begin returns an index (or -1 when disabled)
+int stat_begin(dcsvd_ctx* h, int kind, double work, cudaStream_t st);
+void stat_end(dcsvd_ctx* h, int idx, cudaStream_t st);
 // Read and reset the device status word (synchronizes the stream); maps it
 // to an API status code with a message.
 int check_device_status(dcsvd_ctx* h, cudaStream_t st, const char* stage);

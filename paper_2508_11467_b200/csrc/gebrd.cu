@@ -462,12 +462,20 @@ static int labrd_launch(dcsvd_ctx* h, cudaStream_t st, int mv, int nv, double* A
     return set_error(h, DCSVD_EINVAL, "matrix too large for one LABRD grid (%dx%d)", mv, nv);
   const size_t smem = sizeof(double) * (((CB + 1) & ~1) + (size_t)kLabrdWarps * RB);
   if (smem > 200 * 1024) return set_error(h, DCSVD_EINVAL, "LABRD block too wide (%d columns)", CB);
+  // algorithmic bytes of the two big GEMVs per column:
+  // 8 * sum_k [(mv-k)(nv-k-1) + (mv-k-1)(nv-k-1)]
+  double bytes = 0.0;
+  for (int k = 0; k < nb; ++k) bytes += 8.0 * ((double)(mv - k) * (nv - k - 1) + (double)(mv - k - 1) * (nv - k - 1));
+  const int sidx = stat_begin(h, 0, bytes, st);
+  int rc;
   switch (rpl) {
-    case 2: return launch_labrd<2>(st, la, grid, smem);
-    case 4: return launch_labrd<4>(st, la, grid, smem);
-    case 8: return launch_labrd<8>(st, la, grid, smem);
-    default: return launch_labrd<16>(st, la, grid, smem);
+    case 2: rc = launch_labrd<2>(st, la, grid, smem); break;
+    case 4: rc = launch_labrd<4>(st, la, grid, smem); break;
+    case 8: rc = launch_labrd<8>(st, la, grid, smem); break;
+    default: rc = launch_labrd<16>(st, la, grid, smem); break;
   }
+  stat_end(h, sidx, st);
+  return rc;
 }
 
 int labrd_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A, long long lda, int nb, double* d,

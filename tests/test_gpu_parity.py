@@ -1,0 +1,302 @@
+"""GPU parity: every hot-path entry point on the B200 vs the CPU oracle
+(pinned to the reference by tests/test_oracle_golden.py) and vs the golden
+reference outputs, with the north-star tolerances:
+
+  max|sigma - sigma_ref| / sigma_max        <= 1e-12 * n
+  ||A - U S Vt||_F / (||A||_F * n)          <= 1e-14
+  ||U^T U - I||_F / n, ||V V^T - I||_F / n  <= 1e-14
+
+Intermediate factors (bidiagonal, reflectors, QR) are compared with a
+relative tolerance scaled by ||A|| (floating point, different summation
+order than OpenBLAS)."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+from numpy.testing import assert_array_equal
+
+import oracle
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+pytestmark = pytest.mark.gpu
+
+SIG_TOL = 1e-12
+RES_TOL = 1e-14
+ORTH_TOL = 1e-14
+
+
+def _g():
+    import paper_2508_11467_b200 as g
+
+    return g
+
+
+def check_svd(a, sigma, u, vt, sigma_ref):
+    m, n = a.shape
+    k = min(m, n)
+    nn = max(m, n)
+    smax = max(float(np.max(np.abs(sigma_ref))), np.finfo(float).tiny)
+    assert np.all(np.diff(sigma) <= 0.0) and np.all(sigma >= 0.0)
+    assert np.max(np.abs(sigma - sigma_ref)) / smax <= SIG_TOL * nn
+    if u is not None:
+        na = np.linalg.norm(a)
+        assert np.linalg.norm(a - (u * sigma) @ vt) / (na if na > 0 else 1.0) / nn <= RES_TOL
+        assert np.linalg.norm(u.T @ u - np.eye(k)) / k <= ORTH_TOL
+        assert np.linalg.norm(vt @ vt.T - np.eye(k)) / k <= ORTH_TOL
+
+
+def test_native_library_is_loaded(cuda):
+    g = _g()
+    g.gesdd(np.eye(4))
+    maps = open("/proc/self/maps").read()
+    assert "libdcsvd_b200.so" in maps
+    assert g.launch_count() > 0
+
+
+def test_gesdd_golden_shapes_and_kinds(cuda, golden):
+    g = _g()
+    for i in range(int(golden["svd_count"])):
+        a = golden[f"svd{i}_a"]
+        r = g.gesdd(a)
+        check_svd(a, r.sigma, r.u, r.vt, golden[f"svd{i}_sigma"])
+        v = g.gesdd(a, g.SVDOptions(want_vectors=False))
+        assert v.u is None and v.vt is None
+        assert_array_equal(v.sigma, r.sigma)  # values-only bitwise == vector mode
+
+
+def test_gesdd_input_not_modified(cuda):
+    g = _g()
+    a = oracle.make_matrix("random", 50, 40, seed=3)
+    a0 = a.copy()
+    g.gesdd(a)
+    assert_array_equal(a, a0)
+
+
+def test_gesdd_deterministic(cuda):
+    g = _g()
+    a = oracle.make_matrix("logrand", 300, 200, 1e6, seed=9)
+    r1, r2 = g.gesdd(a), g.gesdd(a)
+    assert_array_equal(r1.sigma, r2.sigma)
+    assert_array_equal(r1.u, r2.u)
+    assert_array_equal(r1.vt, r2.vt)
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (2, 1), (1, 5), (33, 33), (64, 1), (129, 65), (65, 129), (257, 128),
+                                   (500, 100), (100, 500), (600, 64)])
+def test_gesdd_vs_oracle_shapes(cuda, shape):
+    g = _g()
+    m, n = shape
+    a = oracle.make_matrix("random", m, n, seed=m * 7 + n)
+    s, _, _ = oracle.svd(a, want_vectors=False)
+    r = g.gesdd(a)
+    check_svd(a, r.sigma, r.u, r.vt, s)
+
+
+def test_gesdd_rank_deficient_and_zero(cuda):
+    g = _g()
+    rng = np.random.default_rng(4)
+    a = rng.standard_normal((80, 5)) @ rng.standard_normal((5, 60))
+    r = g.gesdd(a)
+    check_svd(a, r.sigma, r.u, r.vt, np.linalg.svd(a, compute_uv=False))
+    z = np.zeros((20, 10))
+    r = g.gesdd(z)
+    assert_array_equal(r.sigma, np.zeros(10))
+    assert np.linalg.norm(r.u.T @ r.u - np.eye(10)) <= 1e-13
+
+
+def test_gesdd_options_paths(cuda):
+    g = _g()
+    a = oracle.make_matrix("geo", 256, 96, 1e10, seed=5)
+    s, _, _ = oracle.svd(a, want_vectors=False)
+    for opts in (g.SVDOptions(), g.SVDOptions(ts_crossover=100.0), g.SVDOptions(leaf_size=4, bidiag_block=8),
+                 g.SVDOptions(apply_block=16, orgqr_block=32, qr_block=8), g.SVDOptions(deflation_multiple=64.0)):
+        r = g.gesdd(a, opts)
+        check_svd(a, r.sigma, r.u, r.vt, s)
+
+
+def test_gesdd_torch_device_path(cuda):
+    g = _g()
+    a = oracle.make_matrix("random", 300, 200, seed=21)
+    t = torch.from_numpy(a).to(cuda)
+    r = g.gesdd(t)
+    assert r.sigma.is_cuda and r.u.is_cuda and r.vt.is_cuda
+    check_svd(a, r.sigma.cpu().numpy(), r.u.cpu().numpy(), r.vt.cpu().numpy(), oracle.svd(a, want_vectors=False)[0])
+
+
+def test_c1_against_reference_sigma(cuda):
+    g = _g()
+    ref = np.load(os.path.join(GOLDEN, "c1_sigma.npz"))
+    a = oracle.make_matrix("random", 1024, 1024, seed=1)
+    r = g.gesdd(a)
+    check_svd(a, r.sigma, r.u, r.vt, ref["sigma"])
+
+
+def test_gebrd_vs_golden(cuda, golden):
+    g = _g()
+    for i in range(int(golden["gebrd_count"])):
+        a = golden[f"gebrd{i}_a"].copy(order="F")
+        f = g.gebrd_blocked(a, int(golden[f"gebrd{i}_block"]))
+        scale = np.linalg.norm(golden[f"gebrd{i}_a"])
+        for name in ("d", "e"):
+            assert np.max(np.abs(getattr(f, name) - golden[f"gebrd{i}_{name}"])) <= 1e-12 * scale
+        for name in ("tauq", "taup"):
+            assert np.max(np.abs(getattr(f, name) - golden[f"gebrd{i}_{name}"])) <= 1e-11
+        assert np.max(np.abs(a - golden[f"gebrd{i}_packed"])) <= 1e-11 * scale
+        assert f.packed is a  # in place, like bidiag.py:204
+        # B's singular values equal A's
+        n = a.shape[1]
+        b = np.diag(f.d) + np.diag(f.e, 1)
+        sa = np.linalg.svd(golden[f"gebrd{i}_a"], compute_uv=False)
+        assert np.max(np.abs(np.linalg.svd(b, compute_uv=False) - sa)) <= 1e-12 * n * sa[0]
+
+
+def test_gebrd_unblocked_and_panel(cuda):
+    g = _g()
+    rng = np.random.default_rng(6)
+    a = np.asfortranarray(rng.standard_normal((40, 30)))
+    a2 = a.copy(order="F")
+    f = g.gebrd_unblocked(a)
+    d, e, tq, tp = oracle.gebd2(a2)
+    assert np.max(np.abs(f.d - d)) <= 1e-12 * np.linalg.norm(a2)
+    # one LABRD panel vs the oracle panel
+    b = np.asfortranarray(rng.standard_normal((90, 70)))
+    b2 = b.copy(order="F")
+    work = g.PanelWorkspace.allocate(90, 70, 8)
+    dd, ee, t1, t2 = (np.zeros(8) for _ in range(4))
+    p, q = g.labrd_panel(b, 8, work, dd, ee, t1, t2)
+    od, oe, o1, o2 = (np.zeros(8) for _ in range(4))
+    P, Q = oracle.labrd(b2, 8, od, oe, o1, o2)
+    sc = np.linalg.norm(b2)
+    assert np.max(np.abs(dd - od)) <= 1e-12 * sc and np.max(np.abs(ee - oe)) <= 1e-12 * sc
+    assert np.max(np.abs(p - P)) <= 1e-11 * sc and np.max(np.abs(q - Q)) <= 1e-11 * sc
+    assert np.max(np.abs(b - b2)) <= 1e-11 * sc
+
+
+def test_qr_vs_golden(cuda, golden):
+    g = _g()
+    for i in range(int(golden["qr_count"])):
+        a = golden[f"qr{i}_a"].copy(order="F")
+        b, ob = (int(x) for x in golden[f"qr{i}_blocks"])
+        f = g.geqrf_blocked(a, b)
+        sc = np.linalg.norm(golden[f"qr{i}_a"])
+        assert np.max(np.abs(a - golden[f"qr{i}_packed"])) <= 1e-12 * sc
+        assert np.max(np.abs(f.tau - golden[f"qr{i}_tau"])) <= 1e-12
+        q = g.orgqr(f, a.shape[1], ob)
+        assert np.max(np.abs(q - golden[f"qr{i}_q"])) <= 1e-12
+
+
+def test_ormbr_vs_oracle(cuda):
+    g = _g()
+    rng = np.random.default_rng(8)
+    for m, n in ((70, 70), (100, 60), (200, 129)):
+        a = np.asfortranarray(rng.standard_normal((m, n)))
+        d, e, tq, tp = oracle.gebrd(a, 32)
+        f = g.BidiagonalFactorization(a, d, e, tq, tp)
+        for trans in (False, True):
+            c = np.asfortranarray(rng.standard_normal((m, 37)))
+            c2 = c.copy(order="F")
+            g.ormqr_like(g.column_reflectors(f), c, transpose=trans)
+            oracle.apply_u1(a, tq, c2, 64, trans=trans)
+            assert np.max(np.abs(c - c2)) <= 1e-12 * np.linalg.norm(c2)
+            v = np.asfortranarray(rng.standard_normal((41, n)))
+            v2 = v.copy(order="F")
+            g.ormlq_like(g.row_reflectors(f), v, transpose=trans)
+            oracle.apply_v1t(a, tp, v2, 64, trans=trans)
+            assert np.max(np.abs(v - v2)) <= 1e-12 * np.linalg.norm(v2)
+
+
+def _bdc_check(g, d, e, bord, leaf, ref_vals=None):
+    prob = g.BidiagonalProblem(d, e, bordered=bord)
+    r = g.bdsdc(prob, leaf=leaf)
+    n = prob.n
+    o = oracle.bdc(oracle.Bidiag(d, e, bord), leaf=leaf)
+    ref = o.vals if ref_vals is None else ref_vals
+    scale = max(float(ref[0]) if n else 1.0, 1.0)
+    if n:
+        assert np.max(np.abs(r.dvals - ref)) <= SIG_TOL * max(n, 1) * scale
+        b = prob.dense()
+        assert np.linalg.norm(b - (r.w * r.dvals) @ r.qfull[:, :n].T) <= 1e-13 * n * scale
+        assert np.linalg.norm(r.w.T @ r.w - np.eye(n)) <= 1e-13 * n
+    assert np.linalg.norm(r.qfull.T @ r.qfull - np.eye(prob.ncols)) <= 1e-13 * max(n, 1)
+    v = g.bdsdc(prob, want_vectors=False, leaf=leaf)
+    assert v.w is None and v.qfull is None
+    assert_array_equal(v.dvals, r.dvals)  # values-only bitwise (bdc.py:14-21)
+    assert_array_equal(v.edge_rows, r.edge_rows)
+    return r
+
+
+def test_bdsdc_vs_golden(cuda, golden):
+    g = _g()
+    for i in range(int(golden["bdc_count"])):
+        bord, leaf = (int(x) for x in golden[f"bdc{i}_meta"])
+        _bdc_check(g, golden[f"bdc{i}_d"], golden[f"bdc{i}_e"], bool(bord), leaf, golden[f"bdc{i}_vals"])
+
+
+@pytest.mark.parametrize("leaf", [1, 2, 4, 32])
+@pytest.mark.parametrize("bordered", [False, True])
+def test_bdsdc_sizes(cuda, leaf, bordered):
+    g = _g()
+    rng = np.random.default_rng(57)
+    for n in (0, 1, 2, 3, 5, 9, 21, 40, 100):
+        if n == 0 and not bordered:
+            continue
+        d = rng.standard_normal(n)
+        e = rng.standard_normal(n if bordered else max(n - 1, 0))
+        _bdc_check(g, d, e, bordered, leaf)
+
+
+def test_bdsdc_deflation_stress(cuda):
+    g = _g()
+    n = 300
+    _bdc_check(g, np.ones(n), np.zeros(n - 1), False, 8)                          # all duplicates
+    _bdc_check(g, np.repeat([1.0, 2.0, 3.0], 100), np.full(n - 1, 1e-9), False, 32)  # clusters
+    dg = np.float_power(10.0, -np.arange(40, dtype=float))
+    _bdc_check(g, dg, 0.5 * dg[:-1], False, 4)                                    # graded
+    c4 = np.load(os.path.join(GOLDEN, "c4_n1024.npz"))
+    r = _bdc_check(g, c4["d"], c4["e"], False, 32, c4["sigma_ref"])
+    assert np.max(np.abs(r.dvals - c4["sigma_prescribed"])) <= 1e-12 * 1024 * 2
+
+
+def test_bdsdc_diagonal_signed_permutation(cuda):
+    g = _g()
+    r = g.bdsdc(g.BidiagonalProblem([3.0, -1.0, 2.0], np.zeros(2)), leaf=1)
+    np.testing.assert_allclose(r.dvals, [3.0, 2.0, 1.0], rtol=1e-15)
+    np.testing.assert_allclose(np.abs(r.w), np.abs(r.qfull), atol=1e-15)
+
+
+def test_errors_map_to_reference_exceptions(cuda):
+    g = _g()
+    with pytest.raises(ValueError):
+        g.gesdd(np.zeros((0, 3)))
+    with pytest.raises(ValueError):
+        g.gebrd_blocked(np.zeros((3, 5)))
+    with pytest.raises(ValueError):
+        g.bdsdc(g.BidiagonalProblem([1.0], np.zeros(0)), leaf=0)
+    with pytest.raises(ValueError):
+        g.geqrf_blocked(np.zeros((3, 5)))
+
+
+def test_matmul_accumulate(cuda):
+    g = _g()
+    rng = np.random.default_rng(1)
+    for (m, n, k, ta, tb) in ((100, 70, 50, False, False), (130, 257, 64, False, True),
+                              (64, 300, 1000, True, False), (33, 17, 9, True, True)):
+        a = rng.standard_normal((k, m) if ta else (m, k))
+        b = rng.standard_normal((n, k) if tb else (k, n))
+        c = np.asfortranarray(rng.standard_normal((m, n)))
+        ref = 0.5 * c + 2.0 * ((a.T if ta else a) @ (b.T if tb else b))
+        g.matmul_accumulate(2.0, a, ta, b, tb, 0.5, c)
+        assert np.max(np.abs(c - ref)) <= 1e-13 * k * np.max(np.abs(ref))
+    c = np.full((4, 4), np.nan, order="F")
+    g.matmul_accumulate(1.0, np.eye(4), False, np.eye(4), False, 0.0, c)  # beta = 0 never reads C
+    assert_array_equal(c, np.eye(4))
+
+
+def test_gesdd_batched(cuda):
+    g = _g()
+    mats = [oracle.make_matrix("random", 128, 128, seed=1000 + i) for i in range(5)]
+    res = g.gesdd_batched(mats)
+    for a, r in zip(mats, res):
+        check_svd(a, r.sigma, r.u, r.vt, np.linalg.svd(a, compute_uv=False))
