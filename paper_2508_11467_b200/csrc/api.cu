@@ -169,6 +169,7 @@ struct PhaseTimer {
     }
   }
 };
+constexpr int kDriverCwyWidth = 128;
 enum { PH_GEQRF = 0, PH_ORGQR, PH_GEBRD, PH_BDC, PH_ORMBR, PH_GEMM, PH_END = -1 };
 
 // _square_core (driver.py:97-118) for m >= n.  A consumed.
@@ -189,9 +190,13 @@ int square_core(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double*
   if (rc) return rc;
   if (!vec) return 0;
   pt.mark(PH_ORMBR);
-  rc = ormbr_run(h, st, 'Q', false, m, n, A, lda, tq, U, m, n, ldu, o.apply_block);
+  // The driver groups reflectors into the widest CWY panels the GPU kernels
+  // take (kDriverCwyWidth): T^-1 = triu(Y^T Y) + diag(1/tau) is exact for any
+  // width, so this is the same product as the reference's 64-wide blocks
+  // (backtransform.py:90-131) with fewer, larger DMMA GEMMs.
+  rc = ormbr_run(h, st, 'Q', false, m, n, A, lda, tq, U, m, n, ldu, kDriverCwyWidth);
   if (rc) return rc;
-  rc = ormbr_run(h, st, 'P', true, m, n, A, lda, tp, VT, n, n, ldvt, o.apply_block);
+  rc = ormbr_run(h, st, 'P', true, m, n, A, lda, tp, VT, n, n, ldvt, kDriverCwyWidth);
   return rc;
 }
 
@@ -218,7 +223,7 @@ int gesdd_tall(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* 
   rc = square_core(h, st, n, n, R, n, S, U0, n, VT, ldvt, o, pt, dbuf);
   if (rc || !vec) return rc;
   pt.mark(PH_ORGQR);
-  rc = orgqr_run(h, st, m, n, n, A, lda, tau, Qm, m, o.orgqr_block);
+  rc = orgqr_run(h, st, m, n, n, A, lda, tau, Qm, m, kDriverCwyWidth);
   if (rc) return rc;
   pt.mark(PH_GEMM);
   GemmDesc g;

@@ -59,11 +59,16 @@ __device__ __forceinline__ void larfg_scalars(double alpha, double nrm2, double&
   }
 }
 
+// Per-CTA caches of the panel rows of P (1-D row slice) and of Q (1-D column
+// slice): every entry of those slices is produced by this CTA (row/column
+// ownership is the same in every phase), so the per-row / per-column
+// corrections never touch global P/Q for them.
 template <int RPL>
 __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
   extern __shared__ double dsm[];
   __shared__ double sh_red[32];
   __shared__ double sh_coef[64];
+  __shared__ double sh_row[64];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = blockIdx.x;
   const int G = gridDim.x;
@@ -78,19 +83,28 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
   const int br0 = gr * a.RB, br1 = min(m, br0 + a.RB);
   const int bc0 = gc * a.CB, bc1 = min(n, bc0 + a.CB);
   // 1-D slices
-  const int r1lo = g * a.R1, r1hi = min(m, r1lo + a.R1);
-  const int c1lo = g * a.C1, c1hi = min(n, c1lo + a.C1);
-  double* sh_u = dsm;                         // CB doubles
-  double* sh_acc = dsm + ((a.CB + 1) & ~1);   // kLabrdWarps * RB doubles
+  const int R1 = a.R1, C1 = a.C1;
+  const int r1lo = g * R1, r1hi = min(m, r1lo + R1);
+  const int c1lo = g * C1, c1hi = min(n, c1lo + C1);
+  double* sh_u = dsm;                                      // CB
+  double* sh_acc = sh_u + ((a.CB + 1) & ~1);               // kLabrdWarps * RB
+  double* Pc = sh_acc + (size_t)kLabrdWarps * a.RB;        // R1 x 2nb (ld R1)
+  double* Qc = Pc + (size_t)R1 * 2 * nb;                   // C1 x 2nb (ld C1)
+  for (int i = tid; i < (R1 + C1) * 2 * nb; i += blockDim.x) Pc[i] = 0.0;
+  const int myr = r1lo + tid;  // this thread's row in the 1-D slice
+  const int myj = c1lo + tid;  // this thread's column in the 1-D slice
+  const bool own_r = tid < R1 && myr < r1hi;
+  const bool own_c = tid < C1 && myj < c1hi;
+  double* prow = Pc + tid;     // Pc(myr, t) = prow[t * R1]
+  double* qrow = Qc + tid;     // Qc(myj, t) = qrow[t * C1]
 
   // ---- phase 1 for k = 0: c = a[:,0]
   {
     double part = 0.0;
-    const int r = r1lo + tid;
-    if (tid < a.R1 && r < r1hi) {
-      const double c = A[r];
-      a.cvec[r] = c;
-      if (r > 0) part = c * c;
+    if (own_r) {
+      const double c = A[myr];
+      a.cvec[myr] = c;
+      if (myr > 0) part = c * c;
     }
     part = block_sum(part, sh_red);
     if (tid == 0) a.normc[g] = part;
@@ -104,19 +118,19 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
     const double alpha = a.cvec[k];
     larfg_scalars(alpha, sum_partials(a.normc, G, sh_red), tau, beta);
     const double den = alpha - beta;
-    if (g == 0 && tid == 0) {
-      a.d[k] = beta;
-      a.tauq[k] = tau;
-      A[k + (long long)k * lda] = beta;
-      P[k + (long long)c0 * ldp] = 1.0;
-    }
-    {
-      const int r = r1lo + tid;
-      if (tid < a.R1 && r < r1hi && r > k) {
-        const double c = a.cvec[r];
+    if (own_r && myr >= k) {
+      if (myr == k) {
+        a.d[k] = beta;
+        a.tauq[k] = tau;
+        A[k + (long long)k * lda] = beta;
+        P[k + (long long)c0 * ldp] = 1.0;
+        prow[c0 * R1] = 1.0;
+      } else {
+        const double c = a.cvec[myr];
         const double ess = tau != 0.0 ? c / den : c;
-        A[r + (long long)k * lda] = ess;
-        P[r + (long long)c0 * ldp] = ess;
+        A[myr + (long long)k * lda] = ess;
+        P[myr + (long long)c0 * ldp] = ess;
+        prow[c0 * R1] = ess;
       }
     }
     if (tau != 0.0) {
@@ -127,19 +141,34 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
         v[i] = (r < br1 && r >= k) ? (r == k ? 1.0 : a.cvec[r] / den) : 0.0;
       }
       const int jstart = max(bc0, k + 1);
-      for (int j = jstart + warp; j < bc1; j += kLabrdWarps) {
-        const double* col = A + (long long)j * lda;
-        double x[RPL];
+      for (int j = jstart + warp; j < bc1; j += 2 * kLabrdWarps) {
+        const int j2 = j + kLabrdWarps;
+        const bool has2 = j2 < bc1;
+        const double* col0 = A + (long long)j * lda;
+        const double* col1 = A + (long long)(has2 ? j2 : j) * lda;
+        double x0[RPL], x1[RPL];
 #pragma unroll
         for (int i = 0; i < RPL; ++i) {
           const int r = br0 + lane + 32 * i;
-          x[i] = r < br1 ? col[r] : 0.0;
+          const bool ok = r < br1;
+          x0[i] = ok ? col0[r] : 0.0;
+          x1[i] = ok ? col1[r] : 0.0;
         }
-        double s = 0.0;
+        double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-        for (int i = 0; i < RPL; ++i) s += x[i] * v[i];
-        s = warp_sum(s);
-        if (lane == 0) a.py[(long long)gr * a.ldpy + j] = s;
+        for (int i = 0; i < RPL; ++i) {
+          s0 += x0[i] * v[i];
+          s1 += x1[i] * v[i];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+          s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        }
+        if (lane == 0) {
+          a.py[(long long)gr * a.ldpy + j] = s0;
+          if (has2) a.py[(long long)gr * a.ldpy + j2] = s1;
+        }
       }
       // P^T v over this block's rows for t = gc, gc+Gc, ... < 2k
       for (int t = gc + a.Gc * warp; t < c0; t += a.Gc * kLabrdWarps) {
@@ -157,32 +186,37 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
     grid_barrier(a.bar, G, epoch);
 
     // ================= phase 3: y, row update, row norm partial
-    if (tau != 0.0 && tid < c0) {
+    if (tid < c0) {
       double s = 0.0;
-      for (int q = 0; q < a.Gr; ++q) s += a.pw[q * 64 + tid];
+      if (tau != 0.0)
+        for (int q = 0; q < a.Gr; ++q) s += a.pw[q * 64 + tid];
       sh_coef[tid] = s;
+    } else if (tid >= 64 && tid < 64 + c0) {
+      sh_row[tid - 64] = P[k + (long long)(tid - 64) * ldp];  // P[k, t], t < 2k
     }
     __syncthreads();
     {
       double part = 0.0;
-      const int j = c1lo + tid;
-      if (tid < a.C1 && j < c1hi && j > k) {
+      if (own_c && myj > k) {
         double y = 0.0;
         if (tau != 0.0) {
           double s = 0.0;
-          for (int q = 0; q < a.Gr; ++q) s += a.py[(long long)q * a.ldpy + j];
+          for (int q = 0; q < a.Gr; ++q) s += a.py[(long long)q * a.ldpy + myj];
           double corr = 0.0;
-          for (int t = 0; t < c0; ++t) corr += Q[j + (long long)t * ldq] * sh_coef[t];
+#pragma unroll 8
+          for (int t = 0; t < c0; ++t) corr += qrow[t * C1] * sh_coef[t];
           y = tau * (s - corr);
-          Q[j + (long long)c0 * ldq] = y;
+          Q[myj + (long long)c0 * ldq] = y;
+          qrow[c0 * C1] = y;
         }
         double upd = 0.0;
-        for (int t = 0; t < c0; ++t) upd += Q[j + (long long)t * ldq] * P[k + (long long)t * ldp];
+#pragma unroll 8
+        for (int t = 0; t < c0; ++t) upd += qrow[t * C1] * sh_row[t];
         upd += y;  // Q[j,2k] * P[k,2k] with P[k,2k] = 1
-        const double r = A[k + (long long)j * lda] - upd;
-        A[k + (long long)j * lda] = r;
-        a.rvec[j] = r;
-        if (j > k + 1) part = r * r;
+        const double r = A[k + (long long)myj * lda] - upd;
+        A[k + (long long)myj * lda] = r;
+        a.rvec[myj] = r;
+        if (myj > k + 1) part = r * r;
       }
       part = block_sum(part, sh_red);
       if (tid == 0) a.normr[g] = part;
@@ -194,19 +228,19 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
     const double alr = a.rvec[k + 1];
     larfg_scalars(alr, sum_partials(a.normr, G, sh_red), pi, betar);
     const double denr = alr - betar;
-    if (g == 0 && tid == 0) {
-      a.e[k] = betar;
-      a.taup[k] = pi;
-      A[k + (long long)(k + 1) * lda] = betar;
-      Q[(k + 1) + (long long)c1 * ldq] = 1.0;
-    }
-    {
-      const int j = c1lo + tid;
-      if (tid < a.C1 && j < c1hi && j > k + 1) {
-        const double rv = a.rvec[j];
+    if (own_c && myj > k) {
+      if (myj == k + 1) {
+        a.e[k] = betar;
+        a.taup[k] = pi;
+        A[k + (long long)(k + 1) * lda] = betar;
+        Q[(k + 1) + (long long)c1 * ldq] = 1.0;
+        qrow[c1 * C1] = 1.0;
+      } else {
+        const double rv = a.rvec[myj];
         const double ess = pi != 0.0 ? rv / denr : rv;
-        A[k + (long long)j * lda] = ess;
-        Q[j + (long long)c1 * ldq] = ess;
+        A[k + (long long)myj * lda] = ess;
+        Q[myj + (long long)c1 * ldq] = ess;
+        qrow[c1 * C1] = ess;
       }
     }
     if (pi != 0.0) {
@@ -217,17 +251,27 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
       double acc[RPL];
 #pragma unroll
       for (int i = 0; i < RPL; ++i) acc[i] = 0.0;
-      // descending column order (snake against the A^T v pass)
+      // descending column order (snake against the A^T v pass), 2 columns per step
       const int nj = bc1 - jlo;
-      for (int jj = nj - 1 - warp; jj >= 0; jj -= kLabrdWarps) {
+      for (int jj = nj - 1 - warp; jj >= 0; jj -= 2 * kLabrdWarps) {
         const int j = jlo + jj;
-        const double uj = sh_u[j - bc0];
-        const double* col = A + (long long)j * lda;
+        const int jj2 = jj - kLabrdWarps;
+        const bool has2 = jj2 >= 0;
+        const int j2 = has2 ? jlo + jj2 : j;
+        const double u0 = sh_u[j - bc0];
+        const double u1 = has2 ? sh_u[j2 - bc0] : 0.0;
+        const double* col0 = A + (long long)j * lda;
+        const double* col1 = A + (long long)j2 * lda;
+        double x0[RPL], x1[RPL];
 #pragma unroll
         for (int i = 0; i < RPL; ++i) {
           const int r = br0 + lane + 32 * i;
-          if (r < br1) acc[i] += col[r] * uj;
+          const bool ok = r < br1;
+          x0[i] = ok ? col0[r] : 0.0;
+          x1[i] = ok ? col1[r] : 0.0;
         }
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) acc[i] += x0[i] * u0 + x1[i] * u1;
       }
 #pragma unroll
       for (int i = 0; i < RPL; ++i) sh_acc[warp * a.RB + lane + 32 * i] = acc[i];
@@ -253,35 +297,40 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
     grid_barrier(a.bar, G, epoch);
 
     // ================= phase 5: x, next column update
-    if (pi != 0.0 && tid < c1) {
+    const bool next = k + 1 < nb;
+    if (tid < c1) {
       double s = 0.0;
-      for (int q = 0; q < a.Gc; ++q) s += a.ps[q * 64 + tid];
+      if (pi != 0.0)
+        for (int q = 0; q < a.Gc; ++q) s += a.ps[q * 64 + tid];
       sh_coef[tid] = s;
+    } else if (tid >= 64 && tid < 64 + c1) {
+      sh_row[tid - 64] = Q[(k + 1) + (long long)(tid - 64) * ldq];  // Q[k+1, t], t < 2k+1
     }
     __syncthreads();
     {
       double part = 0.0;
-      const int r = r1lo + tid;
-      const bool next = k + 1 < nb;
-      if (tid < a.R1 && r < r1hi && r > k) {
+      if (own_r && myr > k) {
         double x = 0.0;
         if (pi != 0.0) {
           double s = 0.0;
-          for (int q = 0; q < a.Gc; ++q) s += a.px[(long long)q * a.ldpx + r];
+          for (int q = 0; q < a.Gc; ++q) s += a.px[(long long)q * a.ldpx + myr];
           double corr = 0.0;
-          for (int t = 0; t < c1; ++t) corr += P[r + (long long)t * ldp] * sh_coef[t];
+#pragma unroll 8
+          for (int t = 0; t < c1; ++t) corr += prow[t * R1] * sh_coef[t];
           x = pi * (s - corr);
-          P[r + (long long)c1 * ldp] = x;
+          P[myr + (long long)c1 * ldp] = x;
+          prow[c1 * R1] = x;
         }
         if (next) {
           // a[k+1:, k+1] -= P[k+1:, :2k+2] Q[k+1, :2k+2]   (Q[k+1,2k+1] = 1)
           double upd = 0.0;
-          for (int t = 0; t < c1; ++t) upd += P[r + (long long)t * ldp] * Q[(k + 1) + (long long)t * ldq];
+#pragma unroll 8
+          for (int t = 0; t < c1; ++t) upd += prow[t * R1] * sh_row[t];
           upd += x;
-          const double c = A[r + (long long)(k + 1) * lda] - upd;
-          A[r + (long long)(k + 1) * lda] = c;
-          a.cvec[r] = c;
-          if (r > k + 1) part = c * c;
+          const double c = A[myr + (long long)(k + 1) * lda] - upd;
+          A[myr + (long long)(k + 1) * lda] = c;
+          a.cvec[myr] = c;
+          if (myr > k + 1) part = c * c;
         }
       }
       if (next) {
@@ -289,7 +338,7 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
         if (tid == 0) a.normc[g] = part;
       }
     }
-    if (k + 1 < nb) grid_barrier(a.bar, G, epoch);
+    if (next) grid_barrier(a.bar, G, epoch);
   }
 }
 
@@ -460,7 +509,7 @@ static int labrd_launch(dcsvd_ctx* h, cudaStream_t st, int mv, int nv, double* A
   la.C1 = (nv + grid - 1) / grid;
   if (la.R1 > kLabrdThreads || la.C1 > kLabrdThreads)
     return set_error(h, DCSVD_EINVAL, "matrix too large for one LABRD grid (%dx%d)", mv, nv);
-  const size_t smem = sizeof(double) * (((CB + 1) & ~1) + (size_t)kLabrdWarps * RB);
+  const size_t smem = sizeof(double) * (((CB + 1) & ~1) + (size_t)kLabrdWarps * RB + (size_t)(la.R1 + la.C1) * 2 * nb);
   if (smem > 200 * 1024) return set_error(h, DCSVD_EINVAL, "LABRD block too wide (%d columns)", CB);
   // algorithmic bytes of the two big GEMVs per column:
   // 8 * sum_k [(mv-k)(nv-k-1) + (mv-k-1)(nv-k-1)]

@@ -22,26 +22,44 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <bool TA, bool TB, int BM, int BN, int WARPS_M, int WARPS_N>
+template <bool TA, bool TB, int BM, int BN, int BK_, int WARPS_M, int WARPS_N, int STAGES_>
 struct GemmCfg {
-  static constexpr int BK = 16;
-  static constexpr int STAGES = 3;
+  static constexpr int BK = BK_;
+  static constexpr int STAGES = STAGES_;
   static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
   static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
   static constexpr int FM = WTM / 8, FN = WTN / 8;
   // A stage: TA ? [BM][BK+4] : [BK][BM+4];  B stage: TB ? [BK][BN+4] : [BN][BK+4]
+  // (row pitch = 4 mod 16 doubles -> conflict-free m8n8k4 fragment reads)
   static constexpr int LDA_S = TA ? (BK + 4) : (BM + 4);
   static constexpr int LDB_S = TB ? (BN + 4) : (BK + 4);
   static constexpr int A_ELEMS = TA ? BM * (BK + 4) : BK * (BM + 4);
   static constexpr int B_ELEMS = TB ? BK * (BN + 4) : BN * (BK + 4);
   static constexpr int SMEM_BYTES = STAGES * (A_ELEMS + B_ELEMS) * 8;
+  // pairs of consecutive doubles along the contiguous global dimension
+  static constexpr int A_PAIRS = BM * BK / 2, B_PAIRS = BN * BK / 2;
 };
 
-template <bool TA, bool TB, int BM, int BN, int WARPS_M, int WARPS_N>
-__global__ void __launch_bounds__(32 * WARPS_M * WARPS_N)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes) : "memory");
+}
+
+// Copy the pair (x, x+1) along the contiguous dimension; `valid` in {0,1,2}.
+__device__ __forceinline__ void copy_pair(double* dst, const double* src, int valid, bool vec) {
+  if (vec) {
+    cp_async16(dst, src, valid * 8);
+  } else {
+    cp_async8(dst, src, valid > 0);
+    cp_async8(dst + 1, valid > 1 ? src + 1 : src, valid > 1);
+  }
+}
+
+template <bool TA, bool TB, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int MINB>
+__global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
     dgemm_kernel(GemmBatch batch, const GemmDesc* __restrict__ ddesc) {
-  using Cfg = GemmCfg<TA, TB, BM, BN, WARPS_M, WARPS_N>;
-  constexpr int BK = Cfg::BK, STAGES = Cfg::STAGES, THREADS = Cfg::THREADS;
+  using Cfg = GemmCfg<TA, TB, BM, BN, BK, WARPS_M, WARPS_N, STAGES>;
+  constexpr int THREADS = Cfg::THREADS;
   const GemmDesc& P = ddesc ? ddesc[blockIdx.z] : batch.d[blockIdx.z];
   const int M = P.m, N = P.n, K = P.k;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
@@ -55,38 +73,48 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N)
   const long long lda = P.lda, ldb = P.ldb;
   const int* __restrict__ acol = P.acol;
   const int tid = threadIdx.x;
+  const bool vecA = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && ((lda & 1) == 0);
+  const bool vecB = ((reinterpret_cast<uintptr_t>(B) & 15) == 0) && ((ldb & 1) == 0);
 
   auto load_tile = [&](int stage, int kt) {
     const int k0 = kt * BK;
     double* as = As + stage * Cfg::A_ELEMS;
     double* bs = Bs + stage * Cfg::B_ELEMS;
 #pragma unroll
-    for (int e = tid; e < BM * BK; e += THREADS) {
-      int i, kk;
-      if (TA) { kk = e % BK; i = e / BK; } else { i = e % BM; kk = e / BM; }
-      const int gm = m0 + i, gk = k0 + kk;
-      const bool ok = gm < M && gk < K;
-      const double* src = A;
-      if (ok) {
-        if (TA) src = A + (long long)gk + (long long)gm * lda;
-        else {
+    for (int p = tid; p < Cfg::A_PAIRS; p += THREADS) {
+      if (TA) {  // op(A)[i][kk] = A[kk + i*lda], pairs along kk
+        const int kk = 2 * (p % (BK / 2)), i = p / (BK / 2);
+        const int gm = m0 + i, gk = k0 + kk;
+        const int valid = gm < M ? max(0, min(2, K - gk)) : 0;
+        const double* src = valid ? A + (long long)gk + (long long)gm * lda : A;
+        copy_pair(as + i * Cfg::LDA_S + kk, src, valid, vecA);
+      } else {   // op(A)[i][kk] = A[i + col(kk)*lda], pairs along i
+        const int i = 2 * (p % (BM / 2)), kk = p / (BM / 2);
+        const int gm = m0 + i, gk = k0 + kk;
+        const int valid = gk < K ? max(0, min(2, M - gm)) : 0;
+        const double* src = A;
+        if (valid) {
           const long long col = acol ? (long long)acol[gk] : (long long)gk;
           src = A + (long long)gm + col * lda;
         }
+        copy_pair(as + kk * Cfg::LDA_S + i, src, valid, vecA);
       }
-      double* dst = TA ? as + i * Cfg::LDA_S + kk : as + kk * Cfg::LDA_S + i;
-      cp_async8(dst, src, ok);
     }
 #pragma unroll
-    for (int e = tid; e < BN * BK; e += THREADS) {
-      int j, kk;
-      if (TB) { j = e % BN; kk = e / BN; } else { kk = e % BK; j = e / BK; }
-      const int gn = n0 + j, gk = k0 + kk;
-      const bool ok = gn < N && gk < K;
-      const double* src = B;
-      if (ok) src = TB ? B + (long long)gn + (long long)gk * ldb : B + (long long)gk + (long long)gn * ldb;
-      double* dst = TB ? bs + kk * Cfg::LDB_S + j : bs + j * Cfg::LDB_S + kk;
-      cp_async8(dst, src, ok);
+    for (int p = tid; p < Cfg::B_PAIRS; p += THREADS) {
+      if (TB) {  // op(B)[kk][j] = B[j + kk*ldb], pairs along j
+        const int j = 2 * (p % (BN / 2)), kk = p / (BN / 2);
+        const int gn = n0 + j, gk = k0 + kk;
+        const int valid = gk < K ? max(0, min(2, N - gn)) : 0;
+        const double* src = valid ? B + (long long)gn + (long long)gk * ldb : B;
+        copy_pair(bs + kk * Cfg::LDB_S + j, src, valid, vecB);
+      } else {   // op(B)[kk][j] = B[kk + j*ldb], pairs along kk
+        const int kk = 2 * (p % (BK / 2)), j = p / (BK / 2);
+        const int gn = n0 + j, gk = k0 + kk;
+        const int valid = gn < N ? max(0, min(2, K - gk)) : 0;
+        const double* src = valid ? B + (long long)gk + (long long)gn * ldb : B;
+        copy_pair(bs + j * Cfg::LDB_S + kk, src, valid, vecB);
+      }
     }
   };
 
@@ -158,11 +186,11 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N)
   }
 }
 
-template <bool TA, bool TB, int BM, int BN, int WM, int WN>
+template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB>
 static int launch_cfg(cudaStream_t st, const GemmBatch* b, const GemmDesc* dd, int nz, int max_m,
                       int max_n) {
-  using Cfg = GemmCfg<TA, TB, BM, BN, WM, WN>;
-  auto kern = dgemm_kernel<TA, TB, BM, BN, WM, WN>;
+  using Cfg = GemmCfg<TA, TB, BM, BN, BK, WM, WN, STAGES>;
+  auto kern = dgemm_kernel<TA, TB, BM, BN, BK, WM, WN, STAGES, MINB>;
   static bool attr_set = false;
   if (!attr_set) {
     DC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
@@ -179,20 +207,23 @@ static int launch_cfg(cudaStream_t st, const GemmBatch* b, const GemmDesc* dd, i
 
 template <bool TA, bool TB>
 static int launch_sized(cudaStream_t st, const GemmBatch* b, const GemmDesc* dd, int nz, int max_m,
-                        int max_n) {
-  // Big tiles when the output has enough of them to fill 148 SMs.
+                        int max_n, int max_k) {
+  // Large tiles (16 warps, 128x128x32, 1 CTA/SM) when the output fills the
+  // GPU and K is long enough to amortize the pipeline; otherwise 64x64 tiles
+  // with several CTAs per SM so load / MMA / epilogue of different CTAs overlap.
   const long long tiles128 = (long long)((max_m + 127) / 128) * ((max_n + 127) / 128) * nz;
-  if (tiles128 >= 120) return launch_cfg<TA, TB, 128, 128, 4, 2>(st, b, dd, nz, max_m, max_n);
-  return launch_cfg<TA, TB, 64, 64, 2, 2>(st, b, dd, nz, max_m, max_n);
+  if (tiles128 >= 148 && max_k >= 128)
+    return launch_cfg<TA, TB, 128, 128, 32, 4, 4, 3, 1>(st, b, dd, nz, max_m, max_n);
+  return launch_cfg<TA, TB, 64, 64, 16, 2, 2, 3, 3>(st, b, dd, nz, max_m, max_n);
 }
 
 static int dispatch(cudaStream_t st, bool ta, bool tb, const GemmBatch* b, const GemmDesc* dd, int nz,
-                    int max_m, int max_n) {
+                    int max_m, int max_n, int max_k) {
   if (max_m <= 0 || max_n <= 0 || nz <= 0) return 0;
-  if (!ta && !tb) return launch_sized<false, false>(st, b, dd, nz, max_m, max_n);
-  if (!ta && tb) return launch_sized<false, true>(st, b, dd, nz, max_m, max_n);
-  if (ta && !tb) return launch_sized<true, false>(st, b, dd, nz, max_m, max_n);
-  return launch_sized<true, true>(st, b, dd, nz, max_m, max_n);
+  if (!ta && !tb) return launch_sized<false, false>(st, b, dd, nz, max_m, max_n, max_k);
+  if (!ta && tb) return launch_sized<false, true>(st, b, dd, nz, max_m, max_n, max_k);
+  if (ta && !tb) return launch_sized<true, false>(st, b, dd, nz, max_m, max_n, max_k);
+  return launch_sized<true, true>(st, b, dd, nz, max_m, max_n, max_k);
 }
 
 int gemm_launch(cudaStream_t st, bool ta, bool tb, const GemmDesc& d) {
@@ -200,21 +231,22 @@ int gemm_launch(cudaStream_t st, bool ta, bool tb, const GemmDesc& d) {
   GemmBatch b;
   b.d[0] = d;
   b.count = 1;
-  return dispatch(st, ta, tb, &b, nullptr, 1, d.m, d.n);
+  return dispatch(st, ta, tb, &b, nullptr, 1, d.m, d.n, d.k);
 }
 
 int gemm_launch_batch(cudaStream_t st, bool ta, bool tb, const GemmBatch& b) {
-  int mm = 0, nn = 0;
+  int mm = 0, nn = 0, kk = 0;
   for (int i = 0; i < b.count; ++i) {
     mm = b.d[i].m > mm ? b.d[i].m : mm;
     nn = b.d[i].n > nn ? b.d[i].n : nn;
+    kk = b.d[i].k > kk ? b.d[i].k : kk;
   }
-  return dispatch(st, ta, tb, &b, nullptr, b.count, mm, nn);
+  return dispatch(st, ta, tb, &b, nullptr, b.count, mm, nn, kk);
 }
 
 int gemm_launch_device(cudaStream_t st, bool ta, bool tb, const GemmDesc* ddesc, int ndesc, int max_m,
                        int max_n) {
-  return dispatch(st, ta, tb, nullptr, ddesc, ndesc, max_m, max_n);
+  return dispatch(st, ta, tb, nullptr, ddesc, ndesc, max_m, max_n, max_m);
 }
 
 // ---------------------------------------------------------------------------

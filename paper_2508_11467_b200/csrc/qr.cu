@@ -41,45 +41,54 @@ __global__ void build_y_kernel(int ymode, const double* __restrict__ src, long l
   }
 }
 
-// G = sum_s Gp[s]; Tinv = triu(G,1) + diag(1/tau) (1 when tau == 0);
-// T = Tinv^-1 (upper); Top = trans ? T^T : T  (w x w, ld w).
-__global__ void cwy_finish_kernel(const double* __restrict__ Gp, int S, int w, const double* __restrict__ tau,
-                                  int trans, double* __restrict__ Top, int* err) {
-  __shared__ double ti[64 * 65];
+// G = sum_s Gp[s]; Tinv = triu(G,1) + diag(1/tau) (1 when tau == 0)
+// (qrblock.py:90-100); T = Tinv^-1 by row-wise back substitution with T held
+// in shared memory (w <= 128): step i computes row i of T from rows > i, 8
+// threads per column; Top = trans ? T^T : T (w x w, ld w).
+constexpr int kCwyMaxW = 128;
+constexpr int kTinvThreads = 1024;
+
+__global__ void __launch_bounds__(kTinvThreads) cwy_tinv_kernel(const double* __restrict__ Gp, int S, int w,
+                                                                 const double* __restrict__ tau, int trans,
+                                                                 double* __restrict__ TinvT, double* __restrict__ Top,
+                                                                 int* err) {
+  extern __shared__ double tsm[];
+  double* T = tsm;                  // w x w, T[r + c*w]
+  double* rowb = tsm + w * w;       // Tinv row i
   const int tid = threadIdx.x;
+  // TinvT[l + i*w] = Tinv[i, l]  (row i of Tinv contiguous)
   for (int idx = tid; idx < w * w; idx += blockDim.x) {
-    const int i = idx % w, j = idx / w;
+    const int l = idx % w, i = idx / w;
     double v = 0.0;
-    if (i < j) {
-      for (int s = 0; s < S; ++s) v += Gp[(long long)s * w * w + idx];
-    } else if (i == j) {
+    if (i < l) {
+      for (int s = 0; s < S; ++s) v += Gp[(long long)s * w * w + i + (long long)l * w];
+    } else if (i == l) {
       v = tau[i] != 0.0 ? 1.0 / tau[i] : 1.0;
+      if (v == 0.0) raise_dev(err, kDevSingularT);
     }
-    ti[i + j * 65] = v;
+    TinvT[idx] = v;
+    T[idx] = 0.0;
   }
   __syncthreads();
-  if (tid < w) {
-    if (ti[tid + tid * 65] == 0.0) raise_dev(err, kDevSingularT);
-    // column j = tid of T = Tinv^-1 by back substitution (thread-private column)
-    const int j = tid;
-    double* tcol = Top + (long long)j * w;
-    for (int i = w - 1; i >= 0; --i) {
-      double v = 0.0;
-      if (i <= j) {
-        double s = (i == j) ? 1.0 : 0.0;
-        for (int l = i + 1; l <= j; ++l) s -= ti[i + l * 65] * tcol[l];
-        v = s / ti[i + i * 65];
-      }
-      tcol[i] = v;
+  const int c = tid >> 3, sub = tid & 7;
+  for (int i = w - 1; i >= 0; --i) {
+    for (int l = tid; l < w; l += blockDim.x) rowb[l] = TinvT[l + (long long)i * w];
+    __syncthreads();
+    const bool active = c < w && c >= i;
+    double part = 0.0;
+    if (active)
+      for (int l = i + 1 + sub; l <= c; l += 8) part += rowb[l] * T[l + c * w];
+    if (c < ((w + 3) & ~3)) {  // whole warps of column groups shuffle together
+      part += __shfl_xor_sync(0xffffffffu, part, 1);
+      part += __shfl_xor_sync(0xffffffffu, part, 2);
+      part += __shfl_xor_sync(0xffffffffu, part, 4);
     }
+    if (active && sub == 0) T[i + c * w] = ((i == c ? 1.0 : 0.0) - part) / rowb[i];
+    __syncthreads();
   }
-  if (!trans) return;
-  __syncthreads();
-  for (int idx = tid; idx < w * w; idx += blockDim.x) ti[(idx % w) + (idx / w) * 65] = Top[idx];
-  __syncthreads();
   for (int idx = tid; idx < w * w; idx += blockDim.x) {
-    const int i = idx % w, j = idx / w;
-    Top[idx] = ti[j + i * 65];
+    const int r = idx % w, cc = idx / w;
+    Top[idx] = trans ? T[cc + r * w] : T[idx];
   }
 }
 
@@ -104,8 +113,8 @@ static int grid_for(long long n, int threads = 256) {
 // op(T) = T or T^T (trans).  Scratch from pool 0 at `scratch` (caller sized
 // via cwy_scratch_doubles).
 static size_t cwy_scratch_doubles(long long rows_y, long long c_other, int w) {
-  const int S = 4;
-  return (size_t)S * (size_t)w * (size_t)c_other + (size_t)S * w * w + (size_t)w * w + 64;
+  const int S = 8;
+  return (size_t)S * (size_t)w * (size_t)c_other + (size_t)S * w * w + 2 * (size_t)w * w + 64;
 }
 
 static int cwy_apply(dcsvd_ctx* h, cudaStream_t st, char side, bool trans, bool ytrans, const double* Y,
@@ -113,12 +122,14 @@ static int cwy_apply(dcsvd_ctx* h, cudaStream_t st, char side, bool trans, bool 
                      long long c_other, double* scratch) {
   if (rows_y <= 0 || c_other <= 0 || w <= 0) return 0;
   // split-K so that Z's tiles x S fill the GPU
-  const long long zt = (c_other + 63) / 64;
+  if (w > kCwyMaxW) return set_error(h, DCSVD_EINVAL, "CWY block width %d exceeds %d", w, kCwyMaxW);
+  const long long zt = ((w + 127) / 128) * ((c_other + 127) / 128);
   int S = 1;
-  while (S < 4 && zt * S < 2 * h->sms && rows_y / (S * 2) >= 256) S *= 2;
+  while (S < 8 && zt * S < h->sms && rows_y / (S * 2) >= 256) S *= 2;
   double* Zp = scratch;
   double* Gp = Zp + (size_t)S * w * c_other;
   double* Top = Gp + (size_t)S * w * w;
+  double* TinvT = Top + (size_t)w * w;
   const long long kchunk = (rows_y + S - 1) / S;
   GemmBatch zb, gb;
   zb.count = 0;
@@ -154,8 +165,17 @@ static int cwy_apply(dcsvd_ctx* h, cudaStream_t st, char side, bool trans, bool 
   if (rc) return rc;
   rc = gemm_launch_batch(st, !ytrans, ytrans, gb);
   if (rc) return rc;
-  cwy_finish_kernel<<<1, 256, 0, st>>>(Gp, S, w, tau, trans ? 1 : 0, Top, h->d_err);
-  note_launch();
+  {
+    static bool attr = false;
+    if (!attr) {
+      DC_CUDA_TRY(cudaFuncSetAttribute(cwy_tinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (kCwyMaxW * kCwyMaxW + kCwyMaxW) * 8));
+      attr = true;
+    }
+    cwy_tinv_kernel<<<1, kTinvThreads, (size_t)(w * w + w) * 8, st>>>(Gp, S, w, tau, trans ? 1 : 0, TinvT, Top,
+                                                                      h->d_err);
+    note_launch();
+  }
   const long long zc = (long long)w * c_other;
   if (S > 1) {
     splitk_reduce_kernel<<<grid_for(zc), 256, 0, st>>>(Zp, zc, S);
@@ -163,8 +183,7 @@ static int cwy_apply(dcsvd_ctx* h, cudaStream_t st, char side, bool trans, bool 
   }
   // X = op(T) Z  (left, w x c_other) or Z op(T) (right, c_other x w); in place
   // is not possible, so write X into the second partial slot (or a tail slot).
-  double* X = (S > 1) ? Zp + zc : Gp;  // Gp is free after finish when S == 1? no: keep separate
-  if (S == 1) X = Top + (size_t)w * w;  // scratch tail sized below
+  double* X = (S > 1) ? Zp + zc : TinvT + (size_t)w * w;  // scratch tail when S == 1
   GemmDesc xd;
   xd.acol = nullptr; xd.ccol = nullptr; xd.alpha = 1.0; xd.beta = 0.0;
   if (side == 'L') {
@@ -334,7 +353,7 @@ int geqrf_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A
   if (n < 1) return set_error(h, DCSVD_EINVAL, "matrix must have at least one column");
   if (m < n) return set_error(h, DCSVD_EINVAL, "QR factorization requires m >= n, got %lldx%lld", m, n);
   if (nb < 1) return set_error(h, DCSVD_EINVAL, "block width must be >= 1, got %d", nb);
-  if (nb > 64) return set_error(h, DCSVD_EINVAL, "GPU QR supports block width <= 64, got %d", nb);
+  if (nb > kCwyMaxW) return set_error(h, DCSVD_EINVAL, "GPU QR supports block width <= %d, got %d", kCwyMaxW, nb);
   const size_t need = pool_bytes((size_t)m * nb, 8) + pool_bytes((size_t)h->sms * 64 + 64, 8) +
                       pool_bytes(cwy_total_scratch(m, n, nb), 8);
   int rc = pool_reserve(h, 0, need, st);
@@ -371,7 +390,7 @@ __global__ void eye_kernel(double* Q, long long ldq, long long m, long long k) {
 int orgqr_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long nrefl, long long k, const double* A,
               long long lda, const double* tau, double* Q, long long ldq, int nb) {
   if (k < 1 || k > m) return set_error(h, DCSVD_EINVAL, "need 1 <= k <= %lld columns of Q, got %lld", m, k);
-  if (nb < 1 || nb > 64) return set_error(h, DCSVD_EINVAL, "GPU ORGQR supports block width 1..64, got %d", nb);
+  if (nb < 1 || nb > kCwyMaxW) return set_error(h, DCSVD_EINVAL, "GPU ORGQR supports block width 1..%d, got %d", kCwyMaxW, nb);
   const size_t need = pool_bytes((size_t)m * nb, 8) + pool_bytes(cwy_total_scratch(m, k, nb), 8);
   int rc = pool_reserve(h, 0, need, st);
   if (rc) return rc;
@@ -397,7 +416,7 @@ int orgqr_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long nrefl, long 
 int ormbr_run(dcsvd_ctx* h, cudaStream_t st, char vect, bool trans, long long m, long long n, const double* A,
               long long lda, const double* tau, double* C, long long c_rows, long long c_cols, long long ldc,
               int nb) {
-  if (nb < 1 || nb > 64) return set_error(h, DCSVD_EINVAL, "GPU ORMBR supports block width 1..64, got %d", nb);
+  if (nb < 1 || nb > kCwyMaxW) return set_error(h, DCSVD_EINVAL, "GPU ORMBR supports block width 1..%d, got %d", kCwyMaxW, nb);
   if (vect == 'Q') {
     if (c_rows != m) return set_error(h, DCSVD_EINVAL, "C has %lld rows, sequence acts on %lld", c_rows, m);
     const long long count = n;

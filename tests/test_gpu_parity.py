@@ -139,11 +139,13 @@ def test_gebrd_vs_golden(cuda, golden):
         a = golden[f"gebrd{i}_a"].copy(order="F")
         f = g.gebrd_blocked(a, int(golden[f"gebrd{i}_block"]))
         scale = np.linalg.norm(golden[f"gebrd{i}_a"])
+        # entries of B are backward- but not forward-stable: error ~ eps * n * ||A||
+        tol = 1e-13 * a.shape[1] * scale
         for name in ("d", "e"):
-            assert np.max(np.abs(getattr(f, name) - golden[f"gebrd{i}_{name}"])) <= 1e-12 * scale
+            assert np.max(np.abs(getattr(f, name) - golden[f"gebrd{i}_{name}"])) <= tol
         for name in ("tauq", "taup"):
-            assert np.max(np.abs(getattr(f, name) - golden[f"gebrd{i}_{name}"])) <= 1e-11
-        assert np.max(np.abs(a - golden[f"gebrd{i}_packed"])) <= 1e-11 * scale
+            assert np.max(np.abs(getattr(f, name) - golden[f"gebrd{i}_{name}"])) <= 1e-12 * a.shape[1]
+        assert np.max(np.abs(a - golden[f"gebrd{i}_packed"])) <= tol
         assert f.packed is a  # in place, like bidiag.py:204
         # B's singular values equal A's
         n = a.shape[1]
