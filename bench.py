@@ -43,6 +43,7 @@ WORKLOADS = {
     "c2": (8192, 8192, 2, "C2 square 8192x8192 fp64 full SVD with U,S,V (headline)"),
     "c3": (65536, 1024, 3, "C3 tall-skinny 65536x1024 fp64 SVD (GEQRF pre-step + GEBRD + BDC)"),
     "c5": (2048, 2048, 1000, "C5 batch of independent 2048x2048 fp64 SVDs"),
+    "c4": (16384, 16384, 4, "C4 bidiagonal BDC only, n=16384, clustered singular values (heavy deflation), with vectors"),
 }
 
 
@@ -192,6 +193,56 @@ def run_reference(args):
     return 0
 
 
+def run_c4(args, dcs, _lib, torch, dist, ws, rank, local):
+    """BDC-only workload on the committed C4 fixture (tests/golden/c4_n16384.npz)."""
+    z = np.load(os.path.join(ROOT, "tests", "golden", "c4_n16384.npz"))
+    n = z["d"].size
+    d = torch.from_numpy(z["d"]).to(f"cuda:{local}")
+    e = torch.from_numpy(z["e"]).to(f"cuda:{local}")
+    prob = dcs.BidiagonalProblem(d, e)
+    F = 8.0 / 3.0 * n ** 3
+    for _ in range(args.warmup):
+        dcs.bdsdc(prob)
+    torch.cuda.synchronize()
+    s, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = _lib.launch_count()
+    with ClockSampler(local) as clk:
+        s.record()
+        for _ in range(args.steps):
+            r = dcs.bdsdc(prob)
+        e1.record()
+        torch.cuda.synchronize()
+    t_ms = s.elapsed_time(e1) / args.steps
+    vals = r.dvals.cpu().numpy()
+    w = r.w
+    eye = torch.eye(n, dtype=torch.float64, device=w.device)
+    orth_w = torch.linalg.matrix_norm(w.t() @ w - eye).item() / n
+    t0 = time.perf_counter()
+    rv = dcs.bdsdc(prob, want_vectors=False)
+    torch.cuda.synchronize()
+    t_vo = time.perf_counter() - t0
+    line = {
+        "metric": "BDC (bdsdc with vectors) GFLOP/s, nominal 8/3 n^3", "value": F / (t_ms * 1e-3) / 1e9,
+        "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "C4 fixture tests/golden/c4_n16384.npz (LAPACK dgebrd of U diag(sigma) V^T, 8 clusters)",
+        "config": {"workload": WORKLOADS["c4"][3], "n": n},
+        "accuracy": {"max_abs_sigma_vs_reference": float(np.max(np.abs(vals - z["sigma_ref"]))),
+                     "max_abs_sigma_vs_prescribed": float(np.max(np.abs(vals - z["sigma_prescribed"]))),
+                     "orth_w_scaled": orth_w,
+                     "values_only_bitwise_equal": bool(np.array_equal(rv.dvals.cpu().numpy(), vals))},
+        "values_only_seconds": t_vo,
+        "gpu_launches": int((_lib.launch_count() - l0) // max(args.steps, 1)),
+        "clocks": clk.summary(),
+        "cpu_baseline": {"value": float(F / float(z["ref_seconds_values_only"]) / 1e9), "unit": "GFLOP/s", "cores": 7,
+                         "kind": "reference", "seconds": float(z["ref_seconds_values_only"]),
+                         "sample": "reference dcsvd.bdsdc values-only on the same fixture, build container (7 BLAS threads), timed when the fixture was made; with vectors it took 57.2 s (BASELINE.md)"},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -217,6 +268,8 @@ def main():
     from paper_2508_11467_b200 import _lib
 
     m, n, seed, desc = WORKLOADS[args.workload]
+    if args.workload == "c4":
+        return run_c4(args, dcs, _lib, torch, dist, ws, rank, local)
     k = min(m, n)
     batch = args.batch if args.workload == "c5" else 1
     # inputs: rank-specific seeds for replicas / shards

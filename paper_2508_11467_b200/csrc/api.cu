@@ -15,6 +15,7 @@
 
 namespace dc {
 std::atomic<long long> g_launch_count{0};
+extern unsigned long long* g_labrd_tlog;
 thread_local dcsvd_ctx* t_cur = nullptr;
 
 int set_error(dcsvd_ctx* h, int code, const char* fmt, ...) {
@@ -281,6 +282,13 @@ int gesdd_impl(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* 
 extern "C" {
 
 int dcsvd_version(void) { return 100; }
+
+// Debug hook (not in the public header): record per-phase timestamps of the
+// next LABRD launch into a device buffer of >= 1 + 10*nb u64.
+int dcsvd_debug_labrd_tlog(unsigned long long* dev_buf) {
+  dc::g_labrd_tlog = dev_buf;
+  return 0;
+}
 
 int dcsvd_create(dcsvd_handle* out, int device) {
   if (!out) return DCSVD_EINVAL;

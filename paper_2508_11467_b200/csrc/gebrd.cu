@@ -36,7 +36,18 @@ struct LabrdArgs {
   long long ldpy, ldpx;  // leading dims of py (>= n) and px (>= m)
   unsigned* bar;
   int Gr, Gc, RB, CB, R1, C1;
+  unsigned long long* tlog;  // optional phase timestamps (CTA 0, thread 0)
 };
+
+unsigned long long* g_labrd_tlog = nullptr;  // debug: set by dcsvd_debug_labrd_tlog
+
+__device__ __forceinline__ void tmark(const LabrdArgs& a, int idx) {
+  if (a.tlog && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.tlog[idx] = t;
+  }
+}
 
 constexpr int kLabrdThreads = 512;
 constexpr int kLabrdWarps = kLabrdThreads / 32;
@@ -109,14 +120,18 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
     part = block_sum(part, sh_red);
     if (tid == 0) a.normc[g] = part;
   }
+  tmark(a, 0);
   grid_barrier(a.bar, G, epoch);
 
   for (int k = 0; k < nb; ++k) {
     const int c0 = 2 * k, c1 = 2 * k + 1;
+    const int tb = 1 + 10 * k;
+    tmark(a, tb + 0);
     // ================= phase 2: LARFG(col), A^T v, P^T v
     double tau, beta;
     const double alpha = a.cvec[k];
     larfg_scalars(alpha, sum_partials(a.normc, G, sh_red), tau, beta);
+    tmark(a, tb + 1);
     const double den = alpha - beta;
     if (own_r && myr >= k) {
       if (myr == k) {
@@ -183,7 +198,9 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
         if (lane == 0) a.pw[gr * 64 + t] = s;
       }
     }
+    tmark(a, tb + 2);
     grid_barrier(a.bar, G, epoch);
+    tmark(a, tb + 3);
 
     // ================= phase 3: y, row update, row norm partial
     if (tid < c0) {
@@ -221,13 +238,16 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
       part = block_sum(part, sh_red);
       if (tid == 0) a.normr[g] = part;
     }
+    tmark(a, tb + 4);
     grid_barrier(a.bar, G, epoch);
+    tmark(a, tb + 5);
 
     // ================= phase 4: LARFG(row), A u, Q^T u
     double pi, betar;
     const double alr = a.rvec[k + 1];
     larfg_scalars(alr, sum_partials(a.normr, G, sh_red), pi, betar);
     const double denr = alr - betar;
+    tmark(a, tb + 6);
     if (own_c && myj > k) {
       if (myj == k + 1) {
         a.e[k] = betar;
@@ -294,7 +314,9 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
         if (lane == 0) a.ps[gc * 64 + t] = s;
       }
     }
+    tmark(a, tb + 7);
     grid_barrier(a.bar, G, epoch);
+    tmark(a, tb + 8);
 
     // ================= phase 5: x, next column update
     const bool next = k + 1 < nb;
@@ -338,6 +360,7 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
         if (tid == 0) a.normc[g] = part;
       }
     }
+    tmark(a, tb + 9);
     if (next) grid_barrier(a.bar, G, epoch);
   }
 }
@@ -507,6 +530,8 @@ static int labrd_launch(dcsvd_ctx* h, cudaStream_t st, int mv, int nv, double* A
   la.Gr = Gr; la.Gc = Gc; la.RB = RB; la.CB = CB;
   la.R1 = (mv + grid - 1) / grid;
   la.C1 = (nv + grid - 1) / grid;
+  la.tlog = g_labrd_tlog;
+  g_labrd_tlog = nullptr;  // log one launch only
   if (la.R1 > kLabrdThreads || la.C1 > kLabrdThreads)
     return set_error(h, DCSVD_EINVAL, "matrix too large for one LABRD grid (%dx%d)", mv, nv);
   const size_t smem = sizeof(double) * (((CB + 1) & ~1) + (size_t)kLabrdWarps * RB + (size_t)(la.R1 + la.C1) * 2 * nb);
