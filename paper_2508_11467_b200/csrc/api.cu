@@ -8,6 +8,8 @@
 #include <algorithm>
 #include <atomic>
 #include <mutex>
+#include <thread>
+#include <vector>
 
 #include "ctx.cuh"
 #include "gemm.cuh"
@@ -318,15 +320,13 @@ int dcsvd_create(dcsvd_handle* out, int device) {
   return 0;
 }
 
+static void free_ctx_resources(dcsvd_ctx* h);
+
 int dcsvd_destroy(dcsvd_handle h) {
   if (!h) return 0;
   cudaSetDevice(h->device);
   cudaDeviceSynchronize();
-  for (auto& p : h->pool)
-    if (p.ptr) cudaFree(p.ptr);
-  cudaFree(h->d_err);
-  cudaFree(h->d_bar);
-  cudaFreeHost(h->h_err);
+  free_ctx_resources(h);
   delete h;
   return 0;
 }
@@ -459,6 +459,40 @@ int dcsvd_gesdd(dcsvd_handle h, int64_t m, int64_t n, double* A, int64_t lda, do
   return 0;
 }
 
+static dcsvd_ctx* make_sub(dcsvd_ctx* h, int sms) {
+  dcsvd_ctx* s = new dcsvd_ctx();
+  s->device = h->device;
+  s->sms = sms;
+  s->coop_ok = h->coop_ok;
+  if (cudaMalloc(&s->d_err, sizeof(int)) != cudaSuccess || cudaMalloc(&s->d_bar, sizeof(unsigned) * kNumBars) != cudaSuccess ||
+      cudaMallocHost(&s->h_err, sizeof(int)) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete s;
+    return nullptr;
+  }
+  cudaMemset(s->d_err, 0, sizeof(int));
+  cudaMemset(s->d_bar, 0, sizeof(unsigned) * kNumBars);
+  return s;
+}
+
+static void free_ctx_resources(dcsvd_ctx* h) {
+  for (auto* s : h->subs) {
+    free_ctx_resources(s);
+    delete s;
+  }
+  h->subs.clear();
+  for (auto& p : h->pool)
+    if (p.ptr) cudaFree(p.ptr);
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  cudaFree(h->d_err);
+  cudaFree(h->d_bar);
+  cudaFreeHost(h->h_err);
+}
+
+// Independent SVDs run concurrently: `conc` host threads each drive one
+// sub-context (own stream, workspace, barrier counters) through its share of
+// the batch; each sub-context's cooperative kernels use sms/conc CTAs, so the
+// matrices in flight partition the GPU.  No data moves between them.
 int dcsvd_gesdd_batched(dcsvd_handle h, int batch, int64_t m, int64_t n, double* const* A, int64_t lda,
                         double* const* Sg, double* const* U, int64_t ldu, double* const* VT, int64_t ldvt,
                         const dcsvd_opts* opts, int concurrency, void* stream) {
@@ -467,14 +501,60 @@ int dcsvd_gesdd_batched(dcsvd_handle h, int batch, int64_t m, int64_t n, double*
   dcsvd_opts o = opts ? *opts : default_opts();
   int rc = validate_opts(h, o);
   if (rc) return rc;
+  if (batch <= 0) return 0;
   cudaStream_t st = S(stream);
-  (void)concurrency;
-  for (int b = 0; b < batch; ++b) {
-    PhaseTimer pt(false, st);
-    rc = gesdd_impl(h, st, m, n, A[b], lda, Sg[b], U ? U[b] : nullptr, ldu, VT ? VT[b] : nullptr, ldvt, o, pt);
-    if (rc) return rc;
+  int conc = concurrency;
+  if (conc <= 0) {
+    const long long k = std::min(m, n);
+    conc = k <= 1024 ? 8 : (k <= 3072 ? 4 : (k <= 6144 ? 2 : 1));
   }
-  return check_device_status(h, st, "gesdd_batched");
+  conc = std::max(1, std::min(conc, std::min(batch, 16)));
+  if (conc == 1) {
+    for (int b = 0; b < batch; ++b) {
+      PhaseTimer pt(false, st);
+      rc = gesdd_impl(h, st, m, n, A[b], lda, Sg[b], U ? U[b] : nullptr, ldu, VT ? VT[b] : nullptr, ldvt, o, pt);
+      if (rc) return rc;
+    }
+    return check_device_status(h, st, "gesdd_batched");
+  }
+  const int sub_sms = std::max(1, h->sms / conc);
+  while ((int)h->subs.size() < conc) {
+    dcsvd_ctx* s = make_sub(h, sub_sms);
+    if (!s) return set_error(h, DCSVD_ECUDA, "could not create a batch sub-context");
+    h->subs.push_back(s);
+  }
+  for (int t = 0; t < conc; ++t) h->subs[t]->sms = sub_sms;
+  // inputs are ready on `st`: sub-streams wait for it
+  cudaEvent_t ready;
+  DC_CUDA_TRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  DC_CUDA_TRY(cudaEventRecord(ready, st));
+  for (int t = 0; t < conc; ++t) DC_CUDA_TRY(cudaStreamWaitEvent(h->subs[t]->own_stream, ready, 0));
+  std::vector<int> codes(conc, 0);
+  std::vector<std::thread> workers;
+  for (int t = 0; t < conc; ++t) {
+    workers.emplace_back([&, t]() {
+      dcsvd_ctx* s = h->subs[t];
+      Guard gg(s);
+      int c = 0;
+      for (int b = t; b < batch && c == 0; b += conc) {
+        PhaseTimer pt(false, s->own_stream);
+        c = gesdd_impl(s, s->own_stream, m, n, A[b], lda, Sg[b], U ? U[b] : nullptr, ldu, VT ? VT[b] : nullptr,
+                       ldvt, o, pt);
+      }
+      if (c == 0) c = check_device_status(s, s->own_stream, "gesdd_batched");
+      codes[t] = c;
+    });
+  }
+  for (auto& w : workers) w.join();
+  cudaEventDestroy(ready);
+  for (int t = 0; t < conc; ++t) {
+    if (codes[t]) {
+      h->last_error = h->subs[t]->last_error;
+      return codes[t];
+    }
+  }
+  // later work on `st` sees the results (all sub-streams were synchronized)
+  return 0;
 }
 
 }  // extern "C"

@@ -75,13 +75,13 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 }
 
 // Grid-wide barrier for cooperative launches: monotone counter, reset by the
-// host before each launch.  `epoch` counts barriers passed by this CTA.
+// host before each launch.  `epoch` counts barriers passed by this CTA.  One
+// release-add per CTA, acquire polling by one thread, then a CTA barrier.
 __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned nblocks, unsigned& epoch) {
   __syncthreads();
   epoch += 1;
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(ctr, 1u);
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
     const unsigned target = epoch * nblocks;
     while (ld_acquire(ctr) < target) {
     }

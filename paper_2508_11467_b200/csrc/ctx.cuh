@@ -12,6 +12,10 @@ struct DevPool {
 };
 
 struct dcsvd_ctx {
+  // concurrent sub-contexts for batched SVDs (own stream, pools, status word,
+  // barrier counters, SM budget); created lazily by dcsvd_gesdd_batched
+  std::vector<dcsvd_ctx*> subs;
+  cudaStream_t own_stream = nullptr;
   int device = 0;
   int sms = 148;
   int coop_ok = 1;

@@ -35,6 +35,7 @@ struct GemmCfg {
   static constexpr int LDB_S = TB ? (BN + 4) : (BK + 4);
   static constexpr int A_ELEMS = TA ? BM * (BK + 4) : BK * (BM + 4);
   static constexpr int B_ELEMS = TB ? BK * (BN + 4) : BN * (BK + 4);
+  static constexpr int C_ELEMS = BM * BN;  // optional C-tile prefetch (beta != 0)
   static constexpr int SMEM_BYTES = STAGES * (A_ELEMS + B_ELEMS) * 8;
   // pairs of consecutive doubles along the contiguous global dimension
   static constexpr int A_PAIRS = BM * BK / 2, B_PAIRS = BN * BK / 2;
@@ -55,7 +56,7 @@ __device__ __forceinline__ void copy_pair(double* dst, const double* src, int va
   }
 }
 
-template <bool TA, bool TB, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int MINB>
+template <bool TA, bool TB, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int MINB, bool PFC>
 __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
     dgemm_kernel(GemmBatch batch, const GemmDesc* __restrict__ ddesc) {
   using Cfg = GemmCfg<TA, TB, BM, BN, BK, WARPS_M, WARPS_N, STAGES>;
@@ -127,6 +128,27 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
 #pragma unroll
     for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+  // C tile prefetch (PFC, beta != 0): issued first so it lands with stage 0
+  // and the read-modify-write epilogue never waits on HBM.
+  double* Cs = smem + STAGES * (Cfg::A_ELEMS + Cfg::B_ELEMS);
+  const bool pfc = PFC && P.beta != 0.0;
+  if (pfc) {
+    const double* C0 = P.C;
+    const long long ldc0 = P.ldc;
+    const bool vecC = !P.ccol && ((reinterpret_cast<uintptr_t>(C0) & 15) == 0) && ((ldc0 & 1) == 0);
+#pragma unroll
+    for (int p = tid; p < BM * BN / 2; p += THREADS) {
+      const int i = 2 * (p % (BM / 2)), j = p / (BM / 2);
+      const int gm = m0 + i, gn = n0 + j;
+      const int valid = gn < N ? max(0, min(2, M - gm)) : 0;
+      const double* src = C0;
+      if (valid) {
+        const long long col = P.ccol ? (long long)P.ccol[gn] : (long long)gn;
+        src = C0 + (long long)gm + col * ldc0;
+      }
+      copy_pair(Cs + i + j * BM, src, valid, vecC);
+    }
+  }
   const int KT = (K + BK - 1) / BK;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
@@ -175,10 +197,11 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
       double* cc = C + col * ldc;
 #pragma unroll
       for (int i = 0; i < Cfg::FM; ++i) {
-        const int gm = m0 + wm * Cfg::WTM + i * 8 + lr;
+        const int lm = wm * Cfg::WTM + i * 8 + lr;
+        const int gm = m0 + lm;
         if (gm < M) {
           double v = alpha * acc[i][j][h];
-          if (beta != 0.0) v += beta * cc[gm];
+          if (beta != 0.0) v += beta * (pfc ? Cs[lm + (gn - n0) * BM] : cc[gm]);
           cc[gm] = v;
         }
       }
@@ -186,20 +209,21 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
   }
 }
 
-template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB>
+template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, bool PFC>
 static int launch_cfg(cudaStream_t st, const GemmBatch* b, const GemmDesc* dd, int nz, int max_m,
                       int max_n) {
   using Cfg = GemmCfg<TA, TB, BM, BN, BK, WM, WN, STAGES>;
-  auto kern = dgemm_kernel<TA, TB, BM, BN, BK, WM, WN, STAGES, MINB>;
+  auto kern = dgemm_kernel<TA, TB, BM, BN, BK, WM, WN, STAGES, MINB, PFC>;
+  constexpr int smem = Cfg::SMEM_BYTES + (PFC ? Cfg::C_ELEMS * 8 : 0);
   static bool attr_set = false;
   if (!attr_set) {
-    DC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+    DC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = true;
   }
   dim3 grid((max_m + BM - 1) / BM, (max_n + BN - 1) / BN, nz);
   GemmBatch empty;
   empty.count = 0;
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(b ? *b : empty, dd);
+  kern<<<grid, Cfg::THREADS, smem, st>>>(b ? *b : empty, dd);
   note_launch();
   DC_CUDA_TRY(cudaGetLastError());
   return 0;
@@ -207,23 +231,25 @@ static int launch_cfg(cudaStream_t st, const GemmBatch* b, const GemmDesc* dd, i
 
 template <bool TA, bool TB>
 static int launch_sized(cudaStream_t st, const GemmBatch* b, const GemmDesc* dd, int nz, int max_m,
-                        int max_n, int max_k) {
+                        int max_n, int max_k, bool beta_nz) {
   // Large tiles (16 warps, 128x128x32, 1 CTA/SM) when the output fills the
   // GPU and K is long enough to amortize the pipeline; otherwise 64x64 tiles
   // with several CTAs per SM so load / MMA / epilogue of different CTAs overlap.
   const long long tiles128 = (long long)((max_m + 127) / 128) * ((max_n + 127) / 128) * nz;
   if (tiles128 >= 148 && max_k >= 128)
-    return launch_cfg<TA, TB, 128, 128, 32, 4, 4, 3, 1>(st, b, dd, nz, max_m, max_n);
-  return launch_cfg<TA, TB, 64, 64, 16, 2, 2, 3, 3>(st, b, dd, nz, max_m, max_n);
+    return launch_cfg<TA, TB, 128, 128, 32, 4, 4, 3, 1, false>(st, b, dd, nz, max_m, max_n);
+  if (beta_nz && max_k <= 64)  // rank-k updates: C read-modify-write dominates -> prefetch C
+    return launch_cfg<TA, TB, 64, 64, 16, 2, 2, 3, 2, true>(st, b, dd, nz, max_m, max_n);
+  return launch_cfg<TA, TB, 64, 64, 16, 2, 2, 3, 3, false>(st, b, dd, nz, max_m, max_n);
 }
 
 static int dispatch(cudaStream_t st, bool ta, bool tb, const GemmBatch* b, const GemmDesc* dd, int nz,
-                    int max_m, int max_n, int max_k) {
+                    int max_m, int max_n, int max_k, bool beta_nz) {
   if (max_m <= 0 || max_n <= 0 || nz <= 0) return 0;
-  if (!ta && !tb) return launch_sized<false, false>(st, b, dd, nz, max_m, max_n, max_k);
-  if (!ta && tb) return launch_sized<false, true>(st, b, dd, nz, max_m, max_n, max_k);
-  if (ta && !tb) return launch_sized<true, false>(st, b, dd, nz, max_m, max_n, max_k);
-  return launch_sized<true, true>(st, b, dd, nz, max_m, max_n, max_k);
+  if (!ta && !tb) return launch_sized<false, false>(st, b, dd, nz, max_m, max_n, max_k, beta_nz);
+  if (!ta && tb) return launch_sized<false, true>(st, b, dd, nz, max_m, max_n, max_k, beta_nz);
+  if (ta && !tb) return launch_sized<true, false>(st, b, dd, nz, max_m, max_n, max_k, beta_nz);
+  return launch_sized<true, true>(st, b, dd, nz, max_m, max_n, max_k, beta_nz);
 }
 
 int gemm_launch(cudaStream_t st, bool ta, bool tb, const GemmDesc& d) {
@@ -231,22 +257,24 @@ int gemm_launch(cudaStream_t st, bool ta, bool tb, const GemmDesc& d) {
   GemmBatch b;
   b.d[0] = d;
   b.count = 1;
-  return dispatch(st, ta, tb, &b, nullptr, 1, d.m, d.n, d.k);
+  return dispatch(st, ta, tb, &b, nullptr, 1, d.m, d.n, d.k, d.beta != 0.0);
 }
 
 int gemm_launch_batch(cudaStream_t st, bool ta, bool tb, const GemmBatch& b) {
   int mm = 0, nn = 0, kk = 0;
+  bool bnz = false;
   for (int i = 0; i < b.count; ++i) {
+    bnz = bnz || b.d[i].beta != 0.0;
     mm = b.d[i].m > mm ? b.d[i].m : mm;
     nn = b.d[i].n > nn ? b.d[i].n : nn;
     kk = b.d[i].k > kk ? b.d[i].k : kk;
   }
-  return dispatch(st, ta, tb, &b, nullptr, b.count, mm, nn, kk);
+  return dispatch(st, ta, tb, &b, nullptr, b.count, mm, nn, kk, bnz);
 }
 
 int gemm_launch_device(cudaStream_t st, bool ta, bool tb, const GemmDesc* ddesc, int ndesc, int max_m,
                        int max_n) {
-  return dispatch(st, ta, tb, nullptr, ddesc, ndesc, max_m, max_n, max_m);
+  return dispatch(st, ta, tb, nullptr, ddesc, ndesc, max_m, max_n, max_m, false);
 }
 
 // ---------------------------------------------------------------------------

@@ -42,53 +42,56 @@ __global__ void build_y_kernel(int ymode, const double* __restrict__ src, long l
 }
 
 // G = sum_s Gp[s]; Tinv = triu(G,1) + diag(1/tau) (1 when tau == 0)
-// (qrblock.py:90-100); T = Tinv^-1 by row-wise back substitution with T held
-// in shared memory (w <= 128): step i computes row i of T from rows > i, 8
-// threads per column; Top = trans ? T^T : T (w x w, ld w).
+// (qrblock.py:90-100), column-major into global scratch.
 constexpr int kCwyMaxW = 128;
-constexpr int kTinvThreads = 1024;
 
-__global__ void __launch_bounds__(kTinvThreads) cwy_tinv_kernel(const double* __restrict__ Gp, int S, int w,
-                                                                 const double* __restrict__ tau, int trans,
-                                                                 double* __restrict__ TinvT, double* __restrict__ Top,
-                                                                 int* err) {
-  extern __shared__ double tsm[];
-  double* T = tsm;                  // w x w, T[r + c*w]
-  double* rowb = tsm + w * w;       // Tinv row i
-  const int tid = threadIdx.x;
-  // TinvT[l + i*w] = Tinv[i, l]  (row i of Tinv contiguous)
-  for (int idx = tid; idx < w * w; idx += blockDim.x) {
-    const int l = idx % w, i = idx / w;
-    double v = 0.0;
-    if (i < l) {
-      for (int s = 0; s < S; ++s) v += Gp[(long long)s * w * w + i + (long long)l * w];
-    } else if (i == l) {
-      v = tau[i] != 0.0 ? 1.0 / tau[i] : 1.0;
-      if (v == 0.0) raise_dev(err, kDevSingularT);
-    }
-    TinvT[idx] = v;
-    T[idx] = 0.0;
+__global__ void cwy_tinv_build_kernel(const double* __restrict__ Gp, int S, int w, const double* __restrict__ tau,
+                                      double* __restrict__ Tinv, int* err) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= w * w) return;
+  const int i = idx % w, l = idx / w;
+  double v = 0.0;
+  if (i < l) {
+    for (int s = 0; s < S; ++s) v += Gp[(long long)s * w * w + idx];
+  } else if (i == l) {
+    v = tau[i] != 0.0 ? 1.0 / tau[i] : 1.0;
+    if (v == 0.0) raise_dev(err, kDevSingularT);
   }
-  __syncthreads();
-  const int c = tid >> 3, sub = tid & 7;
-  for (int i = w - 1; i >= 0; --i) {
-    for (int l = tid; l < w; l += blockDim.x) rowb[l] = TinvT[l + (long long)i * w];
-    __syncthreads();
-    const bool active = c < w && c >= i;
-    double part = 0.0;
-    if (active)
-      for (int l = i + 1 + sub; l <= c; l += 8) part += rowb[l] * T[l + c * w];
-    if (c < ((w + 3) & ~3)) {  // whole warps of column groups shuffle together
-      part += __shfl_xor_sync(0xffffffffu, part, 1);
-      part += __shfl_xor_sync(0xffffffffu, part, 2);
-      part += __shfl_xor_sync(0xffffffffu, part, 4);
+  Tinv[idx] = v;
+}
+
+// T = Tinv^-1, one warp per column c: right-looking back substitution with
+// the column held in registers (lane owns rows lane + 32q).  Top = T or T^T.
+__global__ void cwy_tinv_solve_kernel(const double* __restrict__ Tinv, int w, int trans, double* __restrict__ Top) {
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= w) return;
+  double t[kCwyMaxW / 32];
+#pragma unroll
+  for (int q = 0; q < kCwyMaxW / 32; ++q) t[q] = (lane + 32 * q == c) ? 1.0 : 0.0;
+  for (int i = c; i >= 0; --i) {
+    const double* col = Tinv + (long long)i * w;  // Tinv[:, i]
+    const int qi = i >> 5, li = i & 31;
+    double ti = 0.0;
+#pragma unroll
+    for (int q = 0; q < kCwyMaxW / 32; ++q)
+      if (q == qi) ti = t[q];
+    ti = __shfl_sync(0xffffffffu, ti, li) / col[i];
+#pragma unroll
+    for (int q = 0; q < kCwyMaxW / 32; ++q) {
+      const int l = lane + 32 * q;
+      if (l < i) t[q] -= col[l] * ti;
+      else if (l == i) t[q] = ti;
     }
-    if (active && sub == 0) T[i + c * w] = ((i == c ? 1.0 : 0.0) - part) / rowb[i];
-    __syncthreads();
   }
-  for (int idx = tid; idx < w * w; idx += blockDim.x) {
-    const int r = idx % w, cc = idx / w;
-    Top[idx] = trans ? T[cc + r * w] : T[idx];
+#pragma unroll
+  for (int q = 0; q < kCwyMaxW / 32; ++q) {
+    const int l = lane + 32 * q;
+    if (l < w) {
+      const double v = l <= c ? t[q] : 0.0;
+      if (trans) Top[c + (long long)l * w] = v;  // Top = T^T: Top[c, l] = T[l, c]
+      else Top[l + (long long)c * w] = v;
+    }
   }
 }
 
@@ -165,17 +168,9 @@ static int cwy_apply(dcsvd_ctx* h, cudaStream_t st, char side, bool trans, bool 
   if (rc) return rc;
   rc = gemm_launch_batch(st, !ytrans, ytrans, gb);
   if (rc) return rc;
-  {
-    static bool attr = false;
-    if (!attr) {
-      DC_CUDA_TRY(cudaFuncSetAttribute(cwy_tinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (kCwyMaxW * kCwyMaxW + kCwyMaxW) * 8));
-      attr = true;
-    }
-    cwy_tinv_kernel<<<1, kTinvThreads, (size_t)(w * w + w) * 8, st>>>(Gp, S, w, tau, trans ? 1 : 0, TinvT, Top,
-                                                                      h->d_err);
-    note_launch();
-  }
+  cwy_tinv_build_kernel<<<(w * w + 255) / 256, 256, 0, st>>>(Gp, S, w, tau, TinvT, h->d_err);
+  cwy_tinv_solve_kernel<<<(w + 7) / 8, 256, 0, st>>>(TinvT, w, trans ? 1 : 0, Top);
+  note_launch(2);
   const long long zc = (long long)w * c_other;
   if (S > 1) {
     splitk_reduce_kernel<<<grid_for(zc), 256, 0, st>>>(Zp, zc, S);

@@ -11,7 +11,7 @@ def t(fn, it=5):
     for _ in range(it): fn()
     e.record(); torch.cuda.synchronize(); return s.elapsed_time(e) / it * 1e-3
 res = []
-for (m, n, k, ta, tb) in [(8192, 8192, 8192, 0, 0), (8160, 8160, 64, 0, 1), (64, 8192, 8192, 1, 0), (8192, 8192, 64, 0, 0), (4096, 6900, 3450, 0, 0), (65536, 1024, 1024, 0, 0), (8192, 64, 8192, 0, 0)]:
+for (m, n, k, ta, tb) in [(4096, 8192, 128, 0, 0), (128, 8192, 4096, 1, 0), (128, 8192, 128, 0, 0), (8192, 8192, 8192, 0, 0), (8160, 8160, 64, 0, 1), (64, 8192, 8192, 1, 0), (8192, 8192, 64, 0, 0), (4096, 6900, 3450, 0, 0), (65536, 1024, 1024, 0, 0), (8192, 64, 8192, 0, 0)]:
     A = torch.randn(k if ta else m, m if ta else k, dtype=torch.float64, device="cuda").t().contiguous().t()
     B = torch.randn(n if tb else k, k if tb else n, dtype=torch.float64, device="cuda").t().contiguous().t()
     C = torch.randn(m, n, dtype=torch.float64, device="cuda").t().contiguous().t()
