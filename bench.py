@@ -394,6 +394,8 @@ def main():
             "frac": (achieved / hbm) if achieved else None,
             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
             "traffic": ncu.get("labrd_dram_bytes_per_launch"),
+            "traffic_note": ("ncu --set full capture of " + str(ncu.get("labrd_captured_launch")) + "; algorithmic bytes of that launch = "
+                             + str(ncu.get("labrd_captured_launch_algorithmic_bytes"))) if ncu else None,
             "algorithmic_bytes_per_step": lab_bytes / max(args.steps, 1),
             "launches_per_step": lab_n / max(args.steps, 1),
             "share_of_step": (lab_ms / args.steps) / t_ms if t_ms > 0 else None,
