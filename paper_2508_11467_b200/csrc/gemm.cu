@@ -243,6 +243,198 @@ static int launch_sized(cudaStream_t st, const GemmBatch* b, const GemmDesc* dd,
   return launch_cfg<TA, TB, 64, 64, 16, 2, 2, 3, 3, false>(st, b, dd, nz, max_m, max_n);
 }
 
+
+// ---------------------------------------------------------------------------
+// Streaming rank-k update  C <- alpha * A * op(B) + beta * C  for small K
+// (<= 128): the GEBRD trailing update A -= P Q^T (bidiag.py:195-197) and the
+// CWY updates C -= Y X (qrblock.py:103-119).  Each CTA owns 64-column strips
+// of C: the K x 64 slice of op(B) is loaded once per strip and stays in shared
+// memory while MT-row tiles of A and C stream through a double-buffered
+// cp.async pipeline, so the DMMA pipe works on tile t while tile t+1's A (L2)
+// and C (HBM) are in flight.  Persistent grid, 1 CTA / SM, 8 warps.
+template <bool TB, int KMAX, int MT>
+struct RankkCfg {
+  static constexpr int NW = 64;
+  static constexpr int THREADS = 256;
+  static constexpr int WARPS_M = 2, WARPS_N = 4;
+  static constexpr int WTM = MT / WARPS_M, WTN = NW / WARPS_N;  // 16 columns per warp
+  static constexpr int FM = WTM / 8, FN = WTN / 8;
+  static constexpr int LDB_S = TB ? (NW + 4) : (KMAX + 4);
+  static constexpr int B_ELEMS = TB ? KMAX * (NW + 4) : NW * (KMAX + 4);
+  static constexpr int LDA_S = MT + 4;
+  static constexpr int A_ELEMS = KMAX * (MT + 4);
+  static constexpr int C_ELEMS = NW * MT;
+  static constexpr int SMEM_BYTES = (B_ELEMS + 2 * A_ELEMS + 2 * C_ELEMS) * 8;
+  static constexpr int CHUNK = 8;  // row tiles per work unit
+};
+
+template <bool TB, int KMAX, int MT>
+__global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P) {
+  using Cfg = RankkCfg<TB, KMAX, MT>;
+  constexpr int THREADS = Cfg::THREADS, NW = Cfg::NW;
+  extern __shared__ __align__(16) double smem[];
+  double* Bs = smem;
+  double* As = Bs + Cfg::B_ELEMS;               // 2 buffers
+  double* Cs = As + 2 * Cfg::A_ELEMS;           // 2 buffers
+  const int M = P.m, N = P.n, K = P.k;
+  const double* __restrict__ A = P.A;
+  const double* __restrict__ B = P.B;
+  double* __restrict__ C = P.C;
+  const long long lda = P.lda, ldb = P.ldb, ldc = P.ldc;
+  const double alpha = P.alpha, beta = P.beta;
+  const bool vecA = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && ((lda & 1) == 0);
+  const bool vecB = ((reinterpret_cast<uintptr_t>(B) & 15) == 0) && ((ldb & 1) == 0);
+  const bool vecC = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && ((ldc & 1) == 0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % Cfg::WARPS_M, wn = warp / Cfg::WARPS_M;
+  const int lr = lane >> 2, lc = lane & 3;
+  const int Kp = (K + 3) & ~3;
+  const int strips = (N + NW - 1) / NW;
+  const int tiles = (M + MT - 1) / MT;
+  const int chunks = (tiles + Cfg::CHUNK - 1) / Cfg::CHUNK;
+  const int units = strips * chunks;
+
+  auto load_tile = [&](int buf, int m0, int n0) {
+    double* as = As + buf * Cfg::A_ELEMS;
+    double* cs = Cs + buf * Cfg::C_ELEMS;
+    for (int p = tid; p < MT * Kp / 2; p += THREADS) {  // A: [k][m], pairs along m
+      const int i = 2 * (p % (MT / 2)), kk = p / (MT / 2);
+      const int gm = m0 + i;
+      const int valid = kk < K ? max(0, min(2, M - gm)) : 0;
+      const double* src = valid ? A + (long long)gm + (long long)kk * lda : A;
+      copy_pair(as + kk * Cfg::LDA_S + i, src, valid, vecA);
+    }
+    if (beta != 0.0) {
+      for (int p = tid; p < MT * NW / 2; p += THREADS) {  // C: [n][m], pairs along m
+        const int i = 2 * (p % (MT / 2)), j = p / (MT / 2);
+        const int gm = m0 + i, gn = n0 + j;
+        const int valid = gn < N ? max(0, min(2, M - gm)) : 0;
+        const double* src = valid ? C + (long long)gm + (long long)gn * ldc : C;
+        copy_pair(cs + j * MT + i, src, valid, vecC);
+      }
+    }
+  };
+
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int s = u / chunks, ch = u % chunks;
+    const int n0 = s * NW;
+    const int t0 = ch * Cfg::CHUNK, t1 = min(tiles, t0 + Cfg::CHUNK);
+    // B strip: op(B)[kk][j], kk < Kp, j < 64
+    if (TB) {
+      for (int p = tid; p < Kp * NW / 2; p += THREADS) {  // B[n + k*ldb]: pairs along n
+        const int j = 2 * (p % (NW / 2)), kk = p / (NW / 2);
+        const int gn = n0 + j;
+        const int valid = kk < K ? max(0, min(2, N - gn)) : 0;
+        const double* src = valid ? B + (long long)gn + (long long)kk * ldb : B;
+        copy_pair(Bs + kk * Cfg::LDB_S + j, src, valid, vecB);
+      }
+    } else {
+      for (int p = tid; p < Kp * NW / 2; p += THREADS) {  // B[k + n*ldb]: pairs along k
+        const int kk = 2 * (p % (Kp / 2)), j = p / (Kp / 2);
+        const int gn = n0 + j;
+        const int valid = gn < N ? max(0, min(2, K - kk)) : 0;
+        const double* src = valid ? B + (long long)kk + (long long)gn * ldb : B;
+        copy_pair(Bs + j * Cfg::LDB_S + kk, src, valid, vecB);
+      }
+    }
+    load_tile(0, t0 * MT, n0);
+    cp_async_commit();
+    for (int t = t0; t < t1; ++t) {
+      const int buf = (t - t0) & 1;
+      if (t + 1 < t1) load_tile(buf ^ 1, (t + 1) * MT, n0);
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncthreads();
+      const double* as = As + buf * Cfg::A_ELEMS;
+      const double* cs = Cs + buf * Cfg::C_ELEMS;
+      double acc[Cfg::FM][Cfg::FN][2];
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll 4
+      for (int ks = 0; ks < Kp; ks += 4) {
+        double af[Cfg::FM], bf[Cfg::FN];
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i) af[i] = as[(ks + lc) * Cfg::LDA_S + wm * Cfg::WTM + i * 8 + lr];
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) {
+          const int n = wn * Cfg::WTN + j * 8 + lr;
+          bf[j] = TB ? Bs[(ks + lc) * Cfg::LDB_S + n] : Bs[n * Cfg::LDB_S + ks + lc];
+        }
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < Cfg::FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+      const int m0 = t * MT;
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int ln = wn * Cfg::WTN + j * 8 + lc * 2 + h;
+          const int gn = n0 + ln;
+          if (gn >= N) continue;
+          double* cc = C + (long long)gn * ldc;
+#pragma unroll
+          for (int i = 0; i < Cfg::FM; ++i) {
+            const int lm = wm * Cfg::WTM + i * 8 + lr;
+            const int gm = m0 + lm;
+            if (gm < M) {
+              double v = alpha * acc[i][j][h];
+              if (beta != 0.0) v += beta * cs[ln * MT + lm];
+              cc[gm] = v;
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+}
+
+template <bool TB, int KMAX, int MT>
+static int launch_rankk(cudaStream_t st, const GemmDesc& d, int sms) {
+  using Cfg = RankkCfg<TB, KMAX, MT>;
+  auto kern = rankk_stream_kernel<TB, KMAX, MT>;
+  static bool attr = false;
+  if (!attr) {
+    DC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+    attr = true;
+  }
+  const int strips = (d.n + 63) / 64;
+  const int tiles = (d.m + MT - 1) / MT;
+  const int units = strips * ((tiles + Cfg::CHUNK - 1) / Cfg::CHUNK);
+  const int grid = std::max(1, std::min(units, sms));
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(d);
+  note_launch();
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+static int g_sms = 0;
+static int sm_count() {
+  if (g_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms <= 0) g_sms = 148;
+  }
+  return g_sms;
+}
+
+// Route rank-k updates (K <= 128, large M x N, plain strided operands) to the
+// streaming kernel.  Returns -1 when the shape does not qualify.
+static int try_rankk(cudaStream_t st, bool ta, bool tb, const GemmDesc& d) {
+  if (ta || d.acol || d.ccol || d.k < 1 || d.k > 128 || d.beta == 0.0) return -1;
+  if ((long long)d.m * d.n < (long long)1024 * 1024 || d.m < 256) return -1;
+  const int sms = sm_count();
+  if (d.k <= 64) return tb ? launch_rankk<true, 64, 64>(st, d, sms) : launch_rankk<false, 64, 64>(st, d, sms);
+  return tb ? launch_rankk<true, 128, 32>(st, d, sms) : launch_rankk<false, 128, 32>(st, d, sms);
+}
+
 static int dispatch(cudaStream_t st, bool ta, bool tb, const GemmBatch* b, const GemmDesc* dd, int nz,
                     int max_m, int max_n, int max_k, bool beta_nz) {
   if (max_m <= 0 || max_n <= 0 || nz <= 0) return 0;
@@ -254,6 +446,8 @@ static int dispatch(cudaStream_t st, bool ta, bool tb, const GemmBatch* b, const
 
 int gemm_launch(cudaStream_t st, bool ta, bool tb, const GemmDesc& d) {
   if (d.m <= 0 || d.n <= 0) return 0;
+  const int r = try_rankk(st, ta, tb, d);
+  if (r >= 0) return r;
   GemmBatch b;
   b.d[0] = d;
   b.count = 1;

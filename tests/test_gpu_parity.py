@@ -347,3 +347,21 @@ def test_c2_scale_square_8192(cuda):
     # sigma-interlacing of the Gram matrix via torch.linalg.eigvalsh (fp64)
     s_ref = torch.linalg.eigvalsh(a.t() @ a).clamp_min(0).sqrt().flip(0)
     assert (r.sigma - s_ref).abs().max().item() / s_ref[0].item() <= SIG_TOL * n
+
+
+@pytest.mark.parametrize("k", [1, 37, 64, 100, 128])
+@pytest.mark.parametrize("tb", [False, True])
+def test_rank_k_update_kernel(cuda, k, tb):
+    """Large rank-k updates take the streaming kernel (gemm.cu); compare with
+    a plain torch fp64 product."""
+    g = _g()
+    torch.manual_seed(k)
+    m, n = 2000, 1500
+    a = torch.randn(m, k, dtype=torch.float64, device=cuda)
+    b = torch.randn(n, k, dtype=torch.float64, device=cuda) if tb else torch.randn(k, n, dtype=torch.float64, device=cuda)
+    c = torch.randn(n, m, dtype=torch.float64, device=cuda).t()  # column-major m x n
+    ref = 0.75 * c + (-1.0) * (a @ (b.t() if tb else b))
+    a_cm = a.t().contiguous().t()
+    b_cm = b.t().contiguous().t()
+    g.matmul_accumulate(-1.0, a_cm, False, b_cm, tb, 0.75, c)
+    assert (c - ref).abs().max().item() <= 1e-12 * max(k, 1)
