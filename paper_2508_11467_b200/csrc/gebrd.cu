@@ -59,6 +59,20 @@ __device__ __forceinline__ double sum_partials(const double* p, int cnt, double*
   return block_sum(v, sh);
 }
 
+// Fixed-order sum of `cnt` strided partials, loads issued 16 at a time.
+__device__ __forceinline__ double sum_strided(const double* p, int cnt, long long stride) {
+  double s = 0.0;
+  for (int q0 = 0; q0 < cnt; q0 += 16) {
+    double t[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) t[q] = (q0 + q < cnt) ? p[(long long)(q0 + q) * stride] : 0.0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      if (q0 + q < cnt) s += t[q];
+  }
+  return s;
+}
+
 __device__ __forceinline__ void larfg_scalars(double alpha, double nrm2, double& tau, double& beta) {
   const double xn = sqrt(nrm2);
   if (xn == 0.0) {
@@ -129,6 +143,13 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
     tmark(a, tb + 0);
     // ================= phase 2: LARFG(col), A^T v, P^T v
     double tau, beta;
+    double v[RPL];
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {  // issue the block-row loads before the reduction
+      const int r = br0 + lane + 32 * i;
+      v[i] = (r < br1 && r > k) ? a.cvec[r] : 0.0;
+    }
+    const double cmine = (own_r && myr > k) ? a.cvec[myr] : 0.0;
     const double alpha = a.cvec[k];
     larfg_scalars(alpha, sum_partials(a.normc, G, sh_red), tau, beta);
     tmark(a, tb + 1);
@@ -141,7 +162,7 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
         P[k + (long long)c0 * ldp] = 1.0;
         prow[c0 * R1] = 1.0;
       } else {
-        const double c = a.cvec[myr];
+        const double c = cmine;
         const double ess = tau != 0.0 ? c / den : c;
         A[myr + (long long)k * lda] = ess;
         P[myr + (long long)c0 * ldp] = ess;
@@ -149,11 +170,10 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
       }
     }
     if (tau != 0.0) {
-      double v[RPL];
 #pragma unroll
       for (int i = 0; i < RPL; ++i) {
         const int r = br0 + lane + 32 * i;
-        v[i] = (r < br1 && r >= k) ? (r == k ? 1.0 : a.cvec[r] / den) : 0.0;
+        v[i] = (r == k) ? 1.0 : (r > k ? v[i] / den : 0.0);
       }
       const int jstart = max(bc0, k + 1);
       for (int j = jstart + warp; j < bc1; j += 2 * kLabrdWarps) {
@@ -203,10 +223,14 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
     tmark(a, tb + 3);
 
     // ================= phase 3: y, row update, row norm partial
+    double pys = 0.0, akj = 0.0;
+    if (own_c && myj > k) {  // independent loads first: one L2 round trip
+      akj = A[k + (long long)myj * lda];
+      if (tau != 0.0) pys = sum_strided(a.py + myj, a.Gr, a.ldpy);
+    }
     if (tid < c0) {
       double s = 0.0;
-      if (tau != 0.0)
-        for (int q = 0; q < a.Gr; ++q) s += a.pw[q * 64 + tid];
+      if (tau != 0.0) s = sum_strided(a.pw + tid, a.Gr, 64);
       sh_coef[tid] = s;
     } else if (tid >= 64 && tid < 64 + c0) {
       sh_row[tid - 64] = P[k + (long long)(tid - 64) * ldp];  // P[k, t], t < 2k
@@ -217,8 +241,7 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
       if (own_c && myj > k) {
         double y = 0.0;
         if (tau != 0.0) {
-          double s = 0.0;
-          for (int q = 0; q < a.Gr; ++q) s += a.py[(long long)q * a.ldpy + myj];
+          const double s = pys;
           double corr = 0.0;
 #pragma unroll 8
           for (int t = 0; t < c0; ++t) corr += qrow[t * C1] * sh_coef[t];
@@ -230,7 +253,7 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
 #pragma unroll 8
         for (int t = 0; t < c0; ++t) upd += qrow[t * C1] * sh_row[t];
         upd += y;  // Q[j,2k] * P[k,2k] with P[k,2k] = 1
-        const double r = A[k + (long long)myj * lda] - upd;
+        const double r = akj - upd;
         A[k + (long long)myj * lda] = r;
         a.rvec[myj] = r;
         if (myj > k + 1) part = r * r;
@@ -244,6 +267,14 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
 
     // ================= phase 4: LARFG(row), A u, Q^T u
     double pi, betar;
+    const int jlo4 = max(bc0, k + 1);
+    double rvb[4];  // block-column entries of row k (CB <= 4 * blockDim)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = jlo4 + tid + q * kLabrdThreads;
+      rvb[q] = (j < bc1 && j > k + 1) ? a.rvec[j] : 0.0;
+    }
+    const double rmine = (own_c && myj > k + 1) ? a.rvec[myj] : 0.0;
     const double alr = a.rvec[k + 1];
     larfg_scalars(alr, sum_partials(a.normr, G, sh_red), pi, betar);
     const double denr = alr - betar;
@@ -256,7 +287,7 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
         Q[(k + 1) + (long long)c1 * ldq] = 1.0;
         qrow[c1 * C1] = 1.0;
       } else {
-        const double rv = a.rvec[myj];
+        const double rv = rmine;
         const double ess = pi != 0.0 ? rv / denr : rv;
         A[k + (long long)myj * lda] = ess;
         Q[myj + (long long)c1 * ldq] = ess;
@@ -264,9 +295,12 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
       }
     }
     if (pi != 0.0) {
-      const int jlo = max(bc0, k + 1);
-      for (int j = jlo + tid; j < bc1; j += blockDim.x)
-        sh_u[j - bc0] = (j == k + 1) ? 1.0 : a.rvec[j] / denr;
+      const int jlo = jlo4;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = jlo + tid + q * kLabrdThreads;
+        if (j < bc1) sh_u[j - bc0] = (j == k + 1) ? 1.0 : rvb[q] / denr;
+      }
       __syncthreads();
       double acc[RPL];
 #pragma unroll
@@ -320,10 +354,14 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
 
     // ================= phase 5: x, next column update
     const bool next = k + 1 < nb;
+    double pxs = 0.0, ark = 0.0;
+    if (own_r && myr > k) {
+      if (next) ark = A[myr + (long long)(k + 1) * lda];
+      if (pi != 0.0) pxs = sum_strided(a.px + myr, a.Gc, a.ldpx);
+    }
     if (tid < c1) {
       double s = 0.0;
-      if (pi != 0.0)
-        for (int q = 0; q < a.Gc; ++q) s += a.ps[q * 64 + tid];
+      if (pi != 0.0) s = sum_strided(a.ps + tid, a.Gc, 64);
       sh_coef[tid] = s;
     } else if (tid >= 64 && tid < 64 + c1) {
       sh_row[tid - 64] = Q[(k + 1) + (long long)(tid - 64) * ldq];  // Q[k+1, t], t < 2k+1
@@ -334,8 +372,7 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
       if (own_r && myr > k) {
         double x = 0.0;
         if (pi != 0.0) {
-          double s = 0.0;
-          for (int q = 0; q < a.Gc; ++q) s += a.px[(long long)q * a.ldpx + myr];
+          const double s = pxs;
           double corr = 0.0;
 #pragma unroll 8
           for (int t = 0; t < c1; ++t) corr += prow[t * R1] * sh_coef[t];
@@ -349,7 +386,7 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
 #pragma unroll 8
           for (int t = 0; t < c1; ++t) upd += prow[t * R1] * sh_row[t];
           upd += x;
-          const double c = A[myr + (long long)(k + 1) * lda] - upd;
+          const double c = ark - upd;
           A[myr + (long long)(k + 1) * lda] = c;
           a.cvec[myr] = c;
           if (myr > k + 1) part = c * c;
@@ -535,7 +572,8 @@ static int labrd_launch(dcsvd_ctx* h, cudaStream_t st, int mv, int nv, double* A
   if (la.R1 > kLabrdThreads || la.C1 > kLabrdThreads)
     return set_error(h, DCSVD_EINVAL, "matrix too large for one LABRD grid (%dx%d)", mv, nv);
   const size_t smem = sizeof(double) * (((CB + 1) & ~1) + (size_t)kLabrdWarps * RB + (size_t)(la.R1 + la.C1) * 2 * nb);
-  if (smem > 200 * 1024) return set_error(h, DCSVD_EINVAL, "LABRD block too wide (%d columns)", CB);
+  if (smem > 200 * 1024 || CB > 4 * kLabrdThreads)
+    return set_error(h, DCSVD_EINVAL, "LABRD block too wide (%d columns)", CB);
   // algorithmic bytes of the two big GEMVs per column:
   // 8 * sum_k [(mv-k)(nv-k-1) + (mv-k-1)(nv-k-1)]
   double bytes = 0.0;
