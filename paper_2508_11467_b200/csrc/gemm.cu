@@ -235,9 +235,11 @@ static int launch_sized(cudaStream_t st, const GemmBatch* b, const GemmDesc* dd,
   // Large tiles (16 warps, 128x128x32, 1 CTA/SM) when the output fills the
   // GPU and K is long enough to amortize the pipeline; otherwise 64x64 tiles
   // with several CTAs per SM so load / MMA / epilogue of different CTAs overlap.
-  const long long tiles128 = (long long)((max_m + 127) / 128) * ((max_n + 127) / 128) * nz;
-  if (tiles128 >= 148 && max_k >= 128)
-    return launch_cfg<TA, TB, 128, 128, 32, 4, 4, 3, 1, false>(st, b, dd, nz, max_m, max_n);
+  // 64x128x16 tiles, 4 warps of 32x64, 3 stages, 2 CTAs/SM: two independent
+  // CTAs per SM keep the DMMA pipe fed across each other's barriers.
+  const long long tiles64x128 = (long long)((max_m + 63) / 64) * ((max_n + 127) / 128) * nz;
+  if (tiles64x128 >= 2 * 148 && max_k >= 128)
+    return launch_cfg<TA, TB, 64, 128, 16, 2, 2, 3, 2, false>(st, b, dd, nz, max_m, max_n);
   if (beta_nz && max_k <= 64)  // rank-k updates: C read-modify-write dominates -> prefetch C
     return launch_cfg<TA, TB, 64, 64, 16, 2, 2, 3, 2, true>(st, b, dd, nz, max_m, max_n);
   return launch_cfg<TA, TB, 64, 64, 16, 2, 2, 3, 3, false>(st, b, dd, nz, max_m, max_n);

@@ -30,7 +30,7 @@ struct GemmDesc {
   double alpha, beta;
 };
 
-constexpr int kMaxBatchDesc = 8;
+constexpr int kMaxBatchDesc = 32;
 struct GemmBatch {
   GemmDesc d[kMaxBatchDesc];
   int count;

@@ -115,8 +115,20 @@ static int grid_for(long long n, int threads = 256) {
 // <- (I - Y op(T) Y^T) C.  side 'R': C (nrows x rows_y) <- C (I - Y op(T) Y^T).
 // op(T) = T or T^T (trans).  Scratch from pool 0 at `scratch` (caller sized
 // via cwy_scratch_doubles).
-static size_t cwy_scratch_doubles(long long rows_y, long long c_other, int w) {
-  const int S = 8;
+// Split-K factor for Z = Y^T C (K = rows_y): enough 64x64 tiles x slices for
+// ~3 CTAs per SM, slices of >= 128 rows, partials <= 16M doubles.
+static int cwy_split(int sms, int w, long long c_other, long long rows_y) {
+  // count 64x128 tiles: enough of them (>= 2 per SM) selects the 2-CTA/SM DMMA config
+  const long long zt = ((w + 63) / 64) * ((c_other + 127) / 128);
+  int S = 1;
+  while (S < kMaxBatchDesc && zt * S < 2LL * sms && rows_y / (S * 2) >= 256 &&
+         (long long)(2 * S) * w * c_other <= (16LL << 20))
+    S *= 2;
+  return S;
+}
+
+static size_t cwy_scratch_doubles(int sms, long long rows_y, long long c_other, int w) {
+  const int S = cwy_split(sms, w, c_other, rows_y);
   return (size_t)S * (size_t)w * (size_t)c_other + (size_t)S * w * w + 2 * (size_t)w * w + 64;
 }
 
@@ -126,9 +138,7 @@ static int cwy_apply(dcsvd_ctx* h, cudaStream_t st, char side, bool trans, bool 
   if (rows_y <= 0 || c_other <= 0 || w <= 0) return 0;
   // split-K so that Z's tiles x S fill the GPU
   if (w > kCwyMaxW) return set_error(h, DCSVD_EINVAL, "CWY block width %d exceeds %d", w, kCwyMaxW);
-  const long long zt = ((w + 127) / 128) * ((c_other + 127) / 128);
-  int S = 1;
-  while (S < 8 && zt * S < h->sms && rows_y / (S * 2) >= 256) S *= 2;
+  const int S = cwy_split(h->sms, w, c_other, rows_y);
   double* Zp = scratch;
   double* Gp = Zp + (size_t)S * w * c_other;
   double* Top = Gp + (size_t)S * w * w;
@@ -204,9 +214,9 @@ static int cwy_apply(dcsvd_ctx* h, cudaStream_t st, char side, bool trans, bool 
   return gemm_launch(st, false, /*tb=*/!ytrans, ud);
 }
 
-static size_t cwy_total_scratch(long long rows_y, long long c_other, int w) {
-  // partials (S<=4) + G partials + Top + X (when S == 1)
-  return cwy_scratch_doubles(rows_y, c_other, w) + (size_t)w * c_other + 64;
+static size_t cwy_total_scratch(int sms, long long rows_y, long long c_other, int w) {
+  // Z partials + G partials + Top + Tinv + X (when S == 1)
+  return cwy_scratch_doubles(sms, rows_y, c_other, w) + (size_t)w * c_other + 64;
 }
 
 // ---------------------------------------------------------------------------
@@ -282,10 +292,11 @@ __global__ void __launch_bounds__(kGeqr2Threads, 1) geqr2_coop_kernel(Geqr2Args 
     }
     grid_barrier(a.bar, G, epoch);
     if (tau != 0.0 && j + 1 < w) {
-      if (tid < w && tid > j) {
+      for (int t = j + 1 + warp; t < w; t += nw) {  // warp per column, fixed-order tree
         double s = 0.0;
-        for (int i = 0; i < G; ++i) s += a.part[i * 64 + tid];
-        sh_w[tid] = s;
+        for (int i = lane; i < G; i += 32) s += a.part[i * 64 + t];
+        s = warp_sum(s);
+        if (lane == 0) sh_w[t] = s;
       }
       __syncthreads();
       for (int idx = tid; idx < nr * (w - j - 1); idx += blockDim.x) {
@@ -349,23 +360,41 @@ int geqrf_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A
   if (m < n) return set_error(h, DCSVD_EINVAL, "QR factorization requires m >= n, got %lldx%lld", m, n);
   if (nb < 1) return set_error(h, DCSVD_EINVAL, "block width must be >= 1, got %d", nb);
   if (nb > kCwyMaxW) return set_error(h, DCSVD_EINVAL, "GPU QR supports block width <= %d, got %d", kCwyMaxW, nb);
-  const size_t need = pool_bytes((size_t)m * nb, 8) + pool_bytes((size_t)h->sms * 64 + 64, 8) +
-                      pool_bytes(cwy_total_scratch(m, n, nb), 8);
+  if (nb > 64) return set_error(h, DCSVD_EINVAL, "GPU QR panel width must be <= 64, got %d", nb);
+  // Two-level blocking (same reflectors, LAPACK dgeqrf order): nb-wide panels
+  // are factored and applied inside an outer block of W = nb*ceil(128/nb)
+  // columns; the far trailing matrix then takes one W-wide CWY block (DMMA
+  // GEMMs with K = W instead of K = nb).
+  const int W = std::min(kCwyMaxW, nb * std::max(1, kCwyMaxW / nb));
+  const size_t need = pool_bytes((size_t)m * W, 8) + pool_bytes((size_t)h->sms * 64 + 64, 8) +
+                      pool_bytes(cwy_total_scratch(h->sms, m, n, W), 8);
   int rc = pool_reserve(h, 0, need, st);
   if (rc) return rc;
-  double* Y = pool_take<double>(h, 0, (size_t)m * nb);
+  double* Y = pool_take<double>(h, 0, (size_t)m * W);
   double* part = pool_take<double>(h, 0, (size_t)h->sms * 64 + 64);
-  double* scr = pool_take<double>(h, 0, cwy_total_scratch(m, n, nb));
-  for (long long off = 0; off < n; off += nb) {
-    const int w = (int)std::min<long long>(nb, n - off);
-    const long long rows = m - off;
-    rc = geqr2_launch(h, st, A + off + off * lda, lda, (int)rows, w, tau + off, part);
-    if (rc) return rc;
-    if (off + w < n) {
-      build_y_kernel<<<grid_for(rows * w), 256, 0, st>>>(0, A + off + off * lda, lda, tau + off, (int)rows, w, Y);
+  double* scr = pool_take<double>(h, 0, cwy_total_scratch(h->sms, m, n, W));
+  for (long long off = 0; off < n; off += W) {
+    const int wW = (int)std::min<long long>(W, n - off);
+    for (int ip = 0; ip < wW; ip += nb) {
+      const int w = std::min(nb, wW - ip);
+      const long long o = off + ip;
+      const long long rows = m - o;
+      rc = geqr2_launch(h, st, A + o + o * lda, lda, (int)rows, w, tau + o, part);
+      if (rc) return rc;
+      if (ip + w < wW) {
+        build_y_kernel<<<grid_for(rows * w), 256, 0, st>>>(0, A + o + o * lda, lda, tau + o, (int)rows, w, Y);
+        note_launch();
+        rc = cwy_apply(h, st, 'L', /*trans=*/true, false, Y, rows, tau + o, w, rows, A + o + (o + w) * lda, lda,
+                       wW - ip - w, scr);
+        if (rc) return rc;
+      }
+    }
+    if (off + wW < n) {
+      const long long rows = m - off;
+      build_y_kernel<<<grid_for(rows * wW), 256, 0, st>>>(0, A + off + off * lda, lda, tau + off, (int)rows, wW, Y);
       note_launch();
-      rc = cwy_apply(h, st, 'L', /*trans=*/true, false, Y, rows, tau + off, w, rows, A + off + (off + w) * lda, lda,
-                     n - off - w, scr);
+      rc = cwy_apply(h, st, 'L', /*trans=*/true, false, Y, rows, tau + off, wW, rows, A + off + (off + wW) * lda, lda,
+                     n - off - wW, scr);
       if (rc) return rc;
     }
   }
@@ -386,11 +415,11 @@ int orgqr_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long nrefl, long 
               long long lda, const double* tau, double* Q, long long ldq, int nb) {
   if (k < 1 || k > m) return set_error(h, DCSVD_EINVAL, "need 1 <= k <= %lld columns of Q, got %lld", m, k);
   if (nb < 1 || nb > kCwyMaxW) return set_error(h, DCSVD_EINVAL, "GPU ORGQR supports block width 1..%d, got %d", kCwyMaxW, nb);
-  const size_t need = pool_bytes((size_t)m * nb, 8) + pool_bytes(cwy_total_scratch(m, k, nb), 8);
+  const size_t need = pool_bytes((size_t)m * nb, 8) + pool_bytes(cwy_total_scratch(h->sms, m, k, nb), 8);
   int rc = pool_reserve(h, 0, need, st);
   if (rc) return rc;
   double* Y = pool_take<double>(h, 0, (size_t)m * nb);
-  double* scr = pool_take<double>(h, 0, cwy_total_scratch(m, k, nb));
+  double* scr = pool_take<double>(h, 0, cwy_total_scratch(h->sms, m, k, nb));
   eye_kernel<<<grid_for(m * k), 256, 0, st>>>(Q, ldq, m, k);
   note_launch();
   long long last = ((nrefl - 1) / nb) * nb;
@@ -415,11 +444,11 @@ int ormbr_run(dcsvd_ctx* h, cudaStream_t st, char vect, bool trans, long long m,
   if (vect == 'Q') {
     if (c_rows != m) return set_error(h, DCSVD_EINVAL, "C has %lld rows, sequence acts on %lld", c_rows, m);
     const long long count = n;
-    const size_t need = pool_bytes((size_t)m * nb, 8) + pool_bytes(cwy_total_scratch(m, c_cols, nb), 8);
+    const size_t need = pool_bytes((size_t)m * nb, 8) + pool_bytes(cwy_total_scratch(h->sms, m, c_cols, nb), 8);
     int rc = pool_reserve(h, 0, need, st);
     if (rc) return rc;
     double* Y = pool_take<double>(h, 0, (size_t)m * nb);
-    double* scr = pool_take<double>(h, 0, cwy_total_scratch(m, c_cols, nb));
+    double* scr = pool_take<double>(h, 0, cwy_total_scratch(h->sms, m, c_cols, nb));
     const long long nblk = (count + nb - 1) / nb;
     for (long long b = 0; b < nblk; ++b) {
       const long long bi = trans ? b : nblk - 1 - b;  // U1^T front-to-back, U1 back-to-front
@@ -434,11 +463,11 @@ int ormbr_run(dcsvd_ctx* h, cudaStream_t st, char vect, bool trans, long long m,
   } else if (vect == 'P') {
     if (c_cols != n) return set_error(h, DCSVD_EINVAL, "C has %lld columns, sequence acts on %lld", c_cols, n);
     const long long count = n > 0 ? n - 1 : 0;
-    const size_t need = pool_bytes((size_t)n * nb, 8) + pool_bytes(cwy_total_scratch(n, c_rows, nb), 8);
+    const size_t need = pool_bytes((size_t)n * nb, 8) + pool_bytes(cwy_total_scratch(h->sms, n, c_rows, nb), 8);
     int rc = pool_reserve(h, 0, need, st);
     if (rc) return rc;
     double* Yt = pool_take<double>(h, 0, (size_t)n * nb);
-    double* scr = pool_take<double>(h, 0, cwy_total_scratch(n, c_rows, nb));
+    double* scr = pool_take<double>(h, 0, cwy_total_scratch(h->sms, n, c_rows, nb));
     const long long nblk = (count + nb - 1) / nb;
     for (long long b = 0; b < nblk; ++b) {
       const long long bi = trans ? nblk - 1 - b : b;  // V1^T back-to-front, V1 front-to-back
