@@ -56,9 +56,13 @@ __device__ __forceinline__ void copy_pair(double* dst, const double* src, int va
   }
 }
 
-template <bool TA, bool TB, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int MINB, bool PFC>
+template <bool TA, bool TB, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int MINB, bool PFC,
+          bool VEC, bool GATHER>
 __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
     dgemm_kernel(GemmBatch batch, const GemmDesc* __restrict__ ddesc) {
+  // GATHER (device descriptors of the BDC merges): A columns gathered and C
+  // columns scattered through index lists; compiled away otherwise.
+  constexpr bool gather = GATHER;
   using Cfg = GemmCfg<TA, TB, BM, BN, BK, WARPS_M, WARPS_N, STAGES>;
   constexpr int THREADS = Cfg::THREADS;
   const GemmDesc& P = ddesc ? ddesc[blockIdx.z] : batch.d[blockIdx.z];
@@ -74,8 +78,9 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
   const long long lda = P.lda, ldb = P.ldb;
   const int* __restrict__ acol = P.acol;
   const int tid = threadIdx.x;
-  const bool vecA = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && ((lda & 1) == 0);
-  const bool vecB = ((reinterpret_cast<uintptr_t>(B) & 15) == 0) && ((ldb & 1) == 0);
+  // VEC (host-checked: 16-byte aligned bases, even leading dimensions) selects
+  // 16-byte cp.async for every pair at compile time.
+  constexpr bool vecA = VEC, vecB = VEC;
 
   auto load_tile = [&](int stage, int kt) {
     const int k0 = kt * BK;
@@ -93,11 +98,9 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
         const int i = 2 * (p % (BM / 2)), kk = p / (BM / 2);
         const int gm = m0 + i, gk = k0 + kk;
         const int valid = gk < K ? max(0, min(2, M - gm)) : 0;
-        const double* src = A;
-        if (valid) {
-          const long long col = acol ? (long long)acol[gk] : (long long)gk;
-          src = A + (long long)gm + col * lda;
-        }
+        long long col = gk;
+        if (gather) col = acol[min(gk, K - 1)];
+        const double* src = valid ? A + (long long)gm + col * lda : A;
         copy_pair(as + kk * Cfg::LDA_S + i, src, valid, vecA);
       }
     }
@@ -193,7 +196,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
     for (int h = 0; h < 2; ++h) {
       const int gn = n0 + wn * Cfg::WTN + j * 8 + lc * 2 + h;
       if (gn >= N) continue;
-      const long long col = ccol ? (long long)ccol[gn] : (long long)gn;
+      const long long col = gather ? (long long)ccol[gn] : (long long)gn;
       double* cc = C + col * ldc;
 #pragma unroll
       for (int i = 0; i < Cfg::FM; ++i) {
@@ -209,11 +212,24 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
   }
 }
 
-template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, bool PFC>
-static int launch_cfg(cudaStream_t st, const GemmBatch* b, const GemmDesc* dd, int nz, int max_m,
-                      int max_n) {
+static bool batch_vec_ok(const GemmBatch* b, const GemmDesc* dd) {
+  if (dd || !b) return false;  // device descriptors: alignment unknown on the host
+  for (int i = 0; i < b->count; ++i) {
+    const GemmDesc& d = b->d[i];
+    if ((reinterpret_cast<uintptr_t>(d.A) & 15) || (reinterpret_cast<uintptr_t>(d.B) & 15) || (d.lda & 1) ||
+        (d.ldb & 1))
+      return false;
+    if (d.beta != 0.0 && ((reinterpret_cast<uintptr_t>(d.C) & 15) || (d.ldc & 1) || d.ccol)) return false;
+  }
+  return true;
+}
+
+template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, bool PFC, bool VEC,
+          bool GATHER>
+static int launch_cfg_v(cudaStream_t st, const GemmBatch* b, const GemmDesc* dd, int nz, int max_m,
+                        int max_n) {
   using Cfg = GemmCfg<TA, TB, BM, BN, BK, WM, WN, STAGES>;
-  auto kern = dgemm_kernel<TA, TB, BM, BN, BK, WM, WN, STAGES, MINB, PFC>;
+  auto kern = dgemm_kernel<TA, TB, BM, BN, BK, WM, WN, STAGES, MINB, PFC, VEC, GATHER>;
   constexpr int smem = Cfg::SMEM_BYTES + (PFC ? Cfg::C_ELEMS * 8 : 0);
   static bool attr_set = false;
   if (!attr_set) {
@@ -227,6 +243,19 @@ static int launch_cfg(cudaStream_t st, const GemmBatch* b, const GemmDesc* dd, i
   note_launch();
   DC_CUDA_TRY(cudaGetLastError());
   return 0;
+}
+
+template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, bool PFC>
+static int launch_cfg(cudaStream_t st, const GemmBatch* b, const GemmDesc* dd, int nz, int max_m,
+                      int max_n) {
+  if (dd) {
+    if constexpr (!TA && !PFC)  // BDC merge products only
+      return launch_cfg_v<TA, TB, BM, BN, BK, WM, WN, STAGES, MINB, PFC, false, true>(st, b, dd, nz, max_m, max_n);
+    return -1;
+  }
+  if (batch_vec_ok(b, dd))
+    return launch_cfg_v<TA, TB, BM, BN, BK, WM, WN, STAGES, MINB, PFC, true, false>(st, b, dd, nz, max_m, max_n);
+  return launch_cfg_v<TA, TB, BM, BN, BK, WM, WN, STAGES, MINB, PFC, false, false>(st, b, dd, nz, max_m, max_n);
 }
 
 template <bool TA, bool TB>
@@ -251,44 +280,40 @@ static int launch_sized(cudaStream_t st, const GemmBatch* b, const GemmDesc* dd,
 // (<= 128): the GEBRD trailing update A -= P Q^T (bidiag.py:195-197) and the
 // CWY updates C -= Y X (qrblock.py:103-119).  Each CTA owns 64-column strips
 // of C: the K x 64 slice of op(B) is loaded once per strip and stays in shared
-// memory while MT-row tiles of A and C stream through a double-buffered
-// cp.async pipeline, so the DMMA pipe works on tile t while tile t+1's A (L2)
-// and C (HBM) are in flight.  Persistent grid, 1 CTA / SM, 8 warps.
-template <bool TB, int KMAX, int MT>
+// memory while MT-row tiles of A stream through a double-buffered cp.async
+// pipeline.  Each thread loads its C fragment into registers at the start of
+// a tile, so the HBM latency of the read-modify-write is covered by that
+// tile's DMMAs.  Persistent grid, 1 CTA / SM, 8 warps.
+template <bool TB, int KMAX, int MT, int WARPS_M>
 struct RankkCfg {
   static constexpr int NW = 64;
   static constexpr int THREADS = 256;
-  static constexpr int WARPS_M = 2, WARPS_N = 4;
-  static constexpr int WTM = MT / WARPS_M, WTN = NW / WARPS_N;  // 16 columns per warp
+  static constexpr int WARPS_N = 8 / WARPS_M;
+  static constexpr int WTM = MT / WARPS_M, WTN = NW / WARPS_N;
   static constexpr int FM = WTM / 8, FN = WTN / 8;
   static constexpr int LDB_S = TB ? (NW + 4) : (KMAX + 4);
   static constexpr int B_ELEMS = TB ? KMAX * (NW + 4) : NW * (KMAX + 4);
   static constexpr int LDA_S = MT + 4;
   static constexpr int A_ELEMS = KMAX * (MT + 4);
-  static constexpr int C_ELEMS = NW * MT;
-  static constexpr int SMEM_BYTES = (B_ELEMS + 2 * A_ELEMS + 2 * C_ELEMS) * 8;
+  static constexpr int SMEM_BYTES = (B_ELEMS + 2 * A_ELEMS) * 8;
   static constexpr int CHUNK = 8;  // row tiles per work unit
 };
 
-template <bool TB, int KMAX, int MT>
+template <bool TB, int KMAX, int MT, int WARPS_M, bool VEC>
 __global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P) {
-  using Cfg = RankkCfg<TB, KMAX, MT>;
+  using Cfg = RankkCfg<TB, KMAX, MT, WARPS_M>;
   constexpr int THREADS = Cfg::THREADS, NW = Cfg::NW;
   extern __shared__ __align__(16) double smem[];
   double* Bs = smem;
-  double* As = Bs + Cfg::B_ELEMS;               // 2 buffers
-  double* Cs = As + 2 * Cfg::A_ELEMS;           // 2 buffers
+  double* As = Bs + Cfg::B_ELEMS;  // 2 buffers
   const int M = P.m, N = P.n, K = P.k;
   const double* __restrict__ A = P.A;
   const double* __restrict__ B = P.B;
   double* __restrict__ C = P.C;
   const long long lda = P.lda, ldb = P.ldb, ldc = P.ldc;
   const double alpha = P.alpha, beta = P.beta;
-  const bool vecA = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && ((lda & 1) == 0);
-  const bool vecB = ((reinterpret_cast<uintptr_t>(B) & 15) == 0) && ((ldb & 1) == 0);
-  const bool vecC = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && ((ldc & 1) == 0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp % Cfg::WARPS_M, wn = warp / Cfg::WARPS_M;
+  const int wm = warp % WARPS_M, wn = warp / WARPS_M;
   const int lr = lane >> 2, lc = lane & 3;
   const int Kp = (K + 3) & ~3;
   const int strips = (N + NW - 1) / NW;
@@ -296,24 +321,14 @@ __global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P) {
   const int chunks = (tiles + Cfg::CHUNK - 1) / Cfg::CHUNK;
   const int units = strips * chunks;
 
-  auto load_tile = [&](int buf, int m0, int n0) {
+  auto load_a = [&](int buf, int m0) {
     double* as = As + buf * Cfg::A_ELEMS;
-    double* cs = Cs + buf * Cfg::C_ELEMS;
     for (int p = tid; p < MT * Kp / 2; p += THREADS) {  // A: [k][m], pairs along m
       const int i = 2 * (p % (MT / 2)), kk = p / (MT / 2);
       const int gm = m0 + i;
       const int valid = kk < K ? max(0, min(2, M - gm)) : 0;
       const double* src = valid ? A + (long long)gm + (long long)kk * lda : A;
-      copy_pair(as + kk * Cfg::LDA_S + i, src, valid, vecA);
-    }
-    if (beta != 0.0) {
-      for (int p = tid; p < MT * NW / 2; p += THREADS) {  // C: [n][m], pairs along m
-        const int i = 2 * (p % (MT / 2)), j = p / (MT / 2);
-        const int gm = m0 + i, gn = n0 + j;
-        const int valid = gn < N ? max(0, min(2, M - gm)) : 0;
-        const double* src = valid ? C + (long long)gm + (long long)gn * ldc : C;
-        copy_pair(cs + j * MT + i, src, valid, vecC);
-      }
+      copy_pair(as + kk * Cfg::LDA_S + i, src, valid, VEC);
     }
   };
 
@@ -321,14 +336,13 @@ __global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P) {
     const int s = u / chunks, ch = u % chunks;
     const int n0 = s * NW;
     const int t0 = ch * Cfg::CHUNK, t1 = min(tiles, t0 + Cfg::CHUNK);
-    // B strip: op(B)[kk][j], kk < Kp, j < 64
     if (TB) {
       for (int p = tid; p < Kp * NW / 2; p += THREADS) {  // B[n + k*ldb]: pairs along n
         const int j = 2 * (p % (NW / 2)), kk = p / (NW / 2);
         const int gn = n0 + j;
         const int valid = kk < K ? max(0, min(2, N - gn)) : 0;
         const double* src = valid ? B + (long long)gn + (long long)kk * ldb : B;
-        copy_pair(Bs + kk * Cfg::LDB_S + j, src, valid, vecB);
+        copy_pair(Bs + kk * Cfg::LDB_S + j, src, valid, VEC);
       }
     } else {
       for (int p = tid; p < Kp * NW / 2; p += THREADS) {  // B[k + n*ldb]: pairs along k
@@ -336,19 +350,32 @@ __global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P) {
         const int gn = n0 + j;
         const int valid = gn < N ? max(0, min(2, K - kk)) : 0;
         const double* src = valid ? B + (long long)kk + (long long)gn * ldb : B;
-        copy_pair(Bs + j * Cfg::LDB_S + kk, src, valid, vecB);
+        copy_pair(Bs + j * Cfg::LDB_S + kk, src, valid, VEC);
       }
     }
-    load_tile(0, t0 * MT, n0);
+    load_a(0, t0 * MT);
     cp_async_commit();
     for (int t = t0; t < t1; ++t) {
       const int buf = (t - t0) & 1;
-      if (t + 1 < t1) load_tile(buf ^ 1, (t + 1) * MT, n0);
+      const int m0 = t * MT;
+      // C fragment of this tile into registers (consumed in the epilogue)
+      double cv[Cfg::FM][Cfg::FN][2];
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gn = n0 + wn * Cfg::WTN + j * 8 + lc * 2 + h;
+#pragma unroll
+          for (int i = 0; i < Cfg::FM; ++i) {
+            const int gm = m0 + wm * Cfg::WTM + i * 8 + lr;
+            cv[i][j][h] = (beta != 0.0 && gn < N && gm < M) ? C[(long long)gm + (long long)gn * ldc] : 0.0;
+          }
+        }
+      if (t + 1 < t1) load_a(buf ^ 1, (t + 1) * MT);
       cp_async_commit();
       cp_async_wait<1>();
       __syncthreads();
       const double* as = As + buf * Cfg::A_ELEMS;
-      const double* cs = Cs + buf * Cfg::C_ELEMS;
       double acc[Cfg::FM][Cfg::FN][2];
 #pragma unroll
       for (int i = 0; i < Cfg::FM; ++i)
@@ -369,24 +396,17 @@ __global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P) {
 #pragma unroll
           for (int j = 0; j < Cfg::FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
       }
-      const int m0 = t * MT;
 #pragma unroll
       for (int j = 0; j < Cfg::FN; ++j) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int ln = wn * Cfg::WTN + j * 8 + lc * 2 + h;
-          const int gn = n0 + ln;
+          const int gn = n0 + wn * Cfg::WTN + j * 8 + lc * 2 + h;
           if (gn >= N) continue;
           double* cc = C + (long long)gn * ldc;
 #pragma unroll
           for (int i = 0; i < Cfg::FM; ++i) {
-            const int lm = wm * Cfg::WTM + i * 8 + lr;
-            const int gm = m0 + lm;
-            if (gm < M) {
-              double v = alpha * acc[i][j][h];
-              if (beta != 0.0) v += beta * cs[ln * MT + lm];
-              cc[gm] = v;
-            }
+            const int gm = m0 + wm * Cfg::WTM + i * 8 + lr;
+            if (gm < M) cc[gm] = alpha * acc[i][j][h] + beta * cv[i][j][h];
           }
         }
       }
@@ -397,10 +417,10 @@ __global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P) {
   }
 }
 
-template <bool TB, int KMAX, int MT>
-static int launch_rankk(cudaStream_t st, const GemmDesc& d, int sms) {
-  using Cfg = RankkCfg<TB, KMAX, MT>;
-  auto kern = rankk_stream_kernel<TB, KMAX, MT>;
+template <bool TB, int KMAX, int MT, int WARPS_M, bool VEC>
+static int launch_rankk_v(cudaStream_t st, const GemmDesc& d, int sms) {
+  using Cfg = RankkCfg<TB, KMAX, MT, WARPS_M>;
+  auto kern = rankk_stream_kernel<TB, KMAX, MT, WARPS_M, VEC>;
   static bool attr = false;
   if (!attr) {
     DC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
@@ -414,6 +434,14 @@ static int launch_rankk(cudaStream_t st, const GemmDesc& d, int sms) {
   note_launch();
   DC_CUDA_TRY(cudaGetLastError());
   return 0;
+}
+
+template <bool TB, int KMAX, int MT, int WARPS_M>
+static int launch_rankk(cudaStream_t st, const GemmDesc& d, int sms) {
+  const bool vec = !((reinterpret_cast<uintptr_t>(d.A) & 15) || (reinterpret_cast<uintptr_t>(d.B) & 15) ||
+                     (d.lda & 1) || (d.ldb & 1));
+  if (vec) return launch_rankk_v<TB, KMAX, MT, WARPS_M, true>(st, d, sms);
+  return launch_rankk_v<TB, KMAX, MT, WARPS_M, false>(st, d, sms);
 }
 
 static int g_sms = 0;
@@ -433,8 +461,8 @@ static int try_rankk(cudaStream_t st, bool ta, bool tb, const GemmDesc& d) {
   if (ta || d.acol || d.ccol || d.k < 1 || d.k > 128 || d.beta == 0.0) return -1;
   if ((long long)d.m * d.n < (long long)1024 * 1024 || d.m < 256) return -1;
   const int sms = sm_count();
-  if (d.k <= 64) return tb ? launch_rankk<true, 64, 64>(st, d, sms) : launch_rankk<false, 64, 64>(st, d, sms);
-  return tb ? launch_rankk<true, 128, 32>(st, d, sms) : launch_rankk<false, 128, 32>(st, d, sms);
+  if (d.k <= 64) return tb ? launch_rankk<true, 64, 128, 4>(st, d, sms) : launch_rankk<false, 64, 128, 4>(st, d, sms);
+  return tb ? launch_rankk<true, 128, 64, 2>(st, d, sms) : launch_rankk<false, 128, 64, 2>(st, d, sms);
 }
 
 static int dispatch(cudaStream_t st, bool ta, bool tb, const GemmBatch* b, const GemmDesc* dd, int nz,
