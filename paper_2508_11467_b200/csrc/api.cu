@@ -506,7 +506,7 @@ int dcsvd_gesdd_batched(dcsvd_handle h, int batch, int64_t m, int64_t n, double*
   int conc = concurrency;
   if (conc <= 0) {
     const long long k = std::min(m, n);
-    conc = k <= 1024 ? 8 : (k <= 3072 ? 4 : (k <= 6144 ? 2 : 1));
+    conc = k <= 2560 ? 8 : (k <= 4096 ? 4 : (k <= 6144 ? 2 : 1));
   }
   conc = std::max(1, std::min(conc, std::min(batch, 16)));
   if (conc == 1) {

@@ -37,6 +37,7 @@ struct LabrdArgs {
   unsigned* bar;
   int Gr, Gc, RB, CB, R1, C1;
   unsigned long long* tlog;  // optional phase timestamps (CTA 0, thread 0)
+  int cache_pq;              // P/Q 1-D slices cached in shared memory
 };
 
 unsigned long long* g_labrd_tlog = nullptr;  // debug: set by dcsvd_debug_labrd_tlog
@@ -113,15 +114,29 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
   const int c1lo = g * C1, c1hi = min(n, c1lo + C1);
   double* sh_u = dsm;                                      // CB
   double* sh_acc = sh_u + ((a.CB + 1) & ~1);               // kLabrdWarps * RB
-  double* Pc = sh_acc + (size_t)kLabrdWarps * a.RB;        // R1 x 2nb (ld R1)
-  double* Qc = Pc + (size_t)R1 * 2 * nb;                   // C1 x 2nb (ld C1)
-  for (int i = tid; i < (R1 + C1) * 2 * nb; i += blockDim.x) Pc[i] = 0.0;
   const int myr = r1lo + tid;  // this thread's row in the 1-D slice
   const int myj = c1lo + tid;  // this thread's column in the 1-D slice
   const bool own_r = tid < R1 && myr < r1hi;
   const bool own_c = tid < C1 && myj < c1hi;
-  double* prow = Pc + tid;     // Pc(myr, t) = prow[t * R1]
-  double* qrow = Qc + tid;     // Qc(myj, t) = qrow[t * C1]
+  // P/Q slice caches in shared memory when they fit (a.cache_pq), else the
+  // same accesses go to global P/Q (writes below then hit the same address twice).
+  double* prow;
+  double* qrow;
+  long long pst, qst;
+  if (a.cache_pq) {
+    double* Pc = sh_acc + (size_t)kLabrdWarps * a.RB;        // R1 x 2nb (ld R1)
+    double* Qc = Pc + (size_t)R1 * 2 * nb;                   // C1 x 2nb (ld C1)
+    for (int i = tid; i < (R1 + C1) * 2 * nb; i += blockDim.x) Pc[i] = 0.0;
+    prow = Pc + tid;
+    qrow = Qc + tid;
+    pst = R1;
+    qst = C1;
+  } else {
+    prow = P + myr;
+    qrow = Q + myj;
+    pst = ldp;
+    qst = ldq;
+  }
 
   // ---- phase 1 for k = 0: c = a[:,0]
   {
@@ -160,13 +175,13 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
         a.tauq[k] = tau;
         A[k + (long long)k * lda] = beta;
         P[k + (long long)c0 * ldp] = 1.0;
-        prow[c0 * R1] = 1.0;
+        prow[c0 * pst] = 1.0;
       } else {
         const double c = cmine;
         const double ess = tau != 0.0 ? c / den : c;
         A[myr + (long long)k * lda] = ess;
         P[myr + (long long)c0 * ldp] = ess;
-        prow[c0 * R1] = ess;
+        prow[c0 * pst] = ess;
       }
     }
     if (tau != 0.0) {
@@ -244,14 +259,14 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
           const double s = pys;
           double corr = 0.0;
 #pragma unroll 8
-          for (int t = 0; t < c0; ++t) corr += qrow[t * C1] * sh_coef[t];
+          for (int t = 0; t < c0; ++t) corr += qrow[t * qst] * sh_coef[t];
           y = tau * (s - corr);
           Q[myj + (long long)c0 * ldq] = y;
-          qrow[c0 * C1] = y;
+          qrow[c0 * qst] = y;
         }
         double upd = 0.0;
 #pragma unroll 8
-        for (int t = 0; t < c0; ++t) upd += qrow[t * C1] * sh_row[t];
+        for (int t = 0; t < c0; ++t) upd += qrow[t * qst] * sh_row[t];
         upd += y;  // Q[j,2k] * P[k,2k] with P[k,2k] = 1
         const double r = akj - upd;
         A[k + (long long)myj * lda] = r;
@@ -285,13 +300,13 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
         a.taup[k] = pi;
         A[k + (long long)(k + 1) * lda] = betar;
         Q[(k + 1) + (long long)c1 * ldq] = 1.0;
-        qrow[c1 * C1] = 1.0;
+        qrow[c1 * qst] = 1.0;
       } else {
         const double rv = rmine;
         const double ess = pi != 0.0 ? rv / denr : rv;
         A[k + (long long)myj * lda] = ess;
         Q[myj + (long long)c1 * ldq] = ess;
-        qrow[c1 * C1] = ess;
+        qrow[c1 * qst] = ess;
       }
     }
     if (pi != 0.0) {
@@ -375,16 +390,16 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
           const double s = pxs;
           double corr = 0.0;
 #pragma unroll 8
-          for (int t = 0; t < c1; ++t) corr += prow[t * R1] * sh_coef[t];
+          for (int t = 0; t < c1; ++t) corr += prow[t * pst] * sh_coef[t];
           x = pi * (s - corr);
           P[myr + (long long)c1 * ldp] = x;
-          prow[c1 * R1] = x;
+          prow[c1 * pst] = x;
         }
         if (next) {
           // a[k+1:, k+1] -= P[k+1:, :2k+2] Q[k+1, :2k+2]   (Q[k+1,2k+1] = 1)
           double upd = 0.0;
 #pragma unroll 8
-          for (int t = 0; t < c1; ++t) upd += prow[t * R1] * sh_row[t];
+          for (int t = 0; t < c1; ++t) upd += prow[t * pst] * sh_row[t];
           upd += x;
           const double c = ark - upd;
           A[myr + (long long)(k + 1) * lda] = c;
@@ -571,7 +586,12 @@ static int labrd_launch(dcsvd_ctx* h, cudaStream_t st, int mv, int nv, double* A
   g_labrd_tlog = nullptr;  // log one launch only
   if (la.R1 > kLabrdThreads || la.C1 > kLabrdThreads)
     return set_error(h, DCSVD_EINVAL, "matrix too large for one LABRD grid (%dx%d)", mv, nv);
-  const size_t smem = sizeof(double) * (((CB + 1) & ~1) + (size_t)kLabrdWarps * RB + (size_t)(la.R1 + la.C1) * 2 * nb);
+  size_t smem = sizeof(double) * (((CB + 1) & ~1) + (size_t)kLabrdWarps * RB + (size_t)(la.R1 + la.C1) * 2 * nb);
+  la.cache_pq = 1;
+  if (smem > 200 * 1024) {
+    la.cache_pq = 0;
+    smem = sizeof(double) * (((CB + 1) & ~1) + (size_t)kLabrdWarps * RB);
+  }
   if (smem > 200 * 1024 || CB > 4 * kLabrdThreads)
     return set_error(h, DCSVD_EINVAL, "LABRD block too wide (%d columns)", CB);
   // algorithmic bytes of the two big GEMVs per column:

@@ -365,3 +365,18 @@ def test_rank_k_update_kernel(cuda, k, tb):
     b_cm = b.t().contiguous().t()
     g.matmul_accumulate(-1.0, a_cm, False, b_cm, tb, 0.75, c)
     assert (c - ref).abs().max().item() <= 1e-12 * max(k, 1)
+
+
+def test_gesdd_batched_high_concurrency(cuda):
+    """12 concurrent sub-contexts: each LABRD grid has ~12 CTAs, which takes
+    the global-memory path for the P/Q slice caches."""
+    g = _g()
+    mats = [torch.rand(2048, 2048, dtype=torch.float64, device=cuda).t() for _ in range(12)]
+    res = g.gesdd_batched(mats, concurrency=12)
+    for a, r in zip(mats, res):
+        s_ref = torch.linalg.eigvalsh(a.t() @ a).clamp_min(0).sqrt().flip(0)
+        assert (r.sigma - s_ref).abs().max().item() / s_ref[0].item() <= SIG_TOL * 2048
+        eye = torch.eye(2048, dtype=torch.float64, device=cuda)
+        assert torch.linalg.matrix_norm(r.u.t() @ r.u - eye).item() / 2048 <= ORTH_TOL
+        resid = torch.linalg.matrix_norm(a - (r.u * r.sigma) @ r.vt).item() / torch.linalg.matrix_norm(a).item()
+        assert resid / 2048 <= RES_TOL
