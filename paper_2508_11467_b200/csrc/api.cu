@@ -344,6 +344,25 @@ int dcsvd_set_stats(dcsvd_handle h, int enable) {
   return 0;
 }
 
+// Debug (not in the public header): per-launch records of a kernel family.
+int dcsvd_debug_stat_records(dcsvd_handle h, int kind, double* ms, double* work, int cap) {
+  if (!h) return -1;
+  cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  int c = 0;
+  for (auto& r : h->stats) {
+    if (r.kind != kind) continue;
+    if (c < cap) {
+      float x = 0.f;
+      cudaEventElapsedTime(&x, r.a, r.b);
+      ms[c] = x;
+      work[c] = r.work;
+    }
+    ++c;
+  }
+  return c;
+}
+
 int dcsvd_get_stats(dcsvd_handle h, int kind, double* ms, double* work, long long* launches) {
   if (!h) return DCSVD_EINVAL;
   cudaSetDevice(h->device);

@@ -74,6 +74,21 @@ __device__ __forceinline__ double sum_strided(const double* p, int cnt, long lon
   return s;
 }
 
+// sum_{t < cnt} x[t * stride] * c[t] with four independent partial chains
+// (fixed combination order -> deterministic).
+__device__ __forceinline__ double dot4(const double* x, long long stride, const double* c, int cnt) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int t = 0;
+  for (; t + 4 <= cnt; t += 4) {
+    s0 += x[(t + 0) * stride] * c[t + 0];
+    s1 += x[(t + 1) * stride] * c[t + 1];
+    s2 += x[(t + 2) * stride] * c[t + 2];
+    s3 += x[(t + 3) * stride] * c[t + 3];
+  }
+  for (; t < cnt; ++t) s0 += x[t * stride] * c[t];
+  return (s0 + s1) + (s2 + s3);
+}
+
 __device__ __forceinline__ void larfg_scalars(double alpha, double nrm2, double& tau, double& beta) {
   const double xn = sqrt(nrm2);
   if (xn == 0.0) {
@@ -257,16 +272,12 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
         double y = 0.0;
         if (tau != 0.0) {
           const double s = pys;
-          double corr = 0.0;
-#pragma unroll 8
-          for (int t = 0; t < c0; ++t) corr += qrow[t * qst] * sh_coef[t];
+          const double corr = dot4(qrow, qst, sh_coef, c0);
           y = tau * (s - corr);
           Q[myj + (long long)c0 * ldq] = y;
           qrow[c0 * qst] = y;
         }
-        double upd = 0.0;
-#pragma unroll 8
-        for (int t = 0; t < c0; ++t) upd += qrow[t * qst] * sh_row[t];
+        double upd = dot4(qrow, qst, sh_row, c0);
         upd += y;  // Q[j,2k] * P[k,2k] with P[k,2k] = 1
         const double r = akj - upd;
         A[k + (long long)myj * lda] = r;
@@ -388,18 +399,14 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
         double x = 0.0;
         if (pi != 0.0) {
           const double s = pxs;
-          double corr = 0.0;
-#pragma unroll 8
-          for (int t = 0; t < c1; ++t) corr += prow[t * pst] * sh_coef[t];
+          const double corr = dot4(prow, pst, sh_coef, c1);
           x = pi * (s - corr);
           P[myr + (long long)c1 * ldp] = x;
           prow[c1 * pst] = x;
         }
         if (next) {
           // a[k+1:, k+1] -= P[k+1:, :2k+2] Q[k+1, :2k+2]   (Q[k+1,2k+1] = 1)
-          double upd = 0.0;
-#pragma unroll 8
-          for (int t = 0; t < c1; ++t) upd += prow[t * pst] * sh_row[t];
+          double upd = dot4(prow, pst, sh_row, c1);
           upd += x;
           const double c = ark - upd;
           A[myr + (long long)(k + 1) * lda] = c;
