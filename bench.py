@@ -324,10 +324,12 @@ def main():
     def e2e_step():
         nonlocal h2d, d2h
         h2d = d2h = 0
+        devs = []
         for hb in host:
-            a_dev = hb.to(f"cuda:{local}", non_blocking=True).t()
+            devs.append(hb.to(f"cuda:{local}", non_blocking=True).t())
             h2d += hb.numel() * 8
-            r = dcs.gesdd(a_dev)
+        rs = [dcs.gesdd(devs[0])] if batch == 1 else dcs.gesdd_batched(devs)
+        for r in rs:
             out_s.copy_(r.sigma, non_blocking=True)
             out_u.copy_(r.u.t(), non_blocking=True)
             out_vt.copy_(r.vt.t(), non_blocking=True)
