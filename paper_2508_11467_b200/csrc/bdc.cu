@@ -112,6 +112,11 @@ __device__ __forceinline__ bool leaf_small(double x, double a, double b, double 
   return fabs(x) <= DC_EPS * (fabs(a) + fabs(b)) || fabs(x) <= DC_EPS * bnorm * 1e-3;
 }
 
+// The scalar recurrence (d, e) lives in registers, lane k holding d[k] and
+// e[k]; reads are warp broadcasts (__shfl_sync) and writes are predicated on
+// the owning lane, so every lane follows the identical (warp-uniform) control
+// flow without shared-memory hazards.  Rotations act on the lane's own rows
+// of W / Q in shared memory.
 __global__ void __launch_bounds__(32 * kLeafWarps) bdc_leaf_kernel(const LeafDesc* __restrict__ leaves, int nleaves,
                                                                    const double* __restrict__ din,
                                                                    const double* __restrict__ ein, double* W,
@@ -127,91 +132,86 @@ __global__ void __launch_bounds__(32 * kLeafWarps) bdc_leaf_kernel(const LeafDes
   const int n = L.n, nc = L.n + L.bordered, r0 = L.r0;
   double* Ws = S.W;
   double* Qs = S.Q;
-  // identity bases
+  constexpr unsigned FULL = 0xffffffffu;
   for (int c = 0; c < n; ++c)
     for (int r = lane; r < n; r += 32) Ws[r + c * kLdW] = (r == c) ? 1.0 : 0.0;
   for (int c = 0; c < nc; ++c)
     for (int r = lane; r < nc; r += 32) Qs[r + c * kLdQ] = (r == c) ? 1.0 : 0.0;
-  if (lane < n) {
-    S.d[lane] = din[r0 + lane];
-    S.e[lane] = ein[r0 + lane];
-  }
-  __syncwarp();
-  double* d = S.d;
-  double* e = S.e;
+  double dr = lane < n ? din[r0 + lane] : 0.0;
+  double er = lane < n ? ein[r0 + lane] : 0.0;
+  auto D = [&](int k) { return __shfl_sync(FULL, dr, k); };
+  auto E = [&](int k) { return __shfl_sync(FULL, er, k); };
+  auto setD = [&](int k, double v) { if (lane == k) dr = v; };
+  auto setE = [&](int k, double v) { if (lane == k) er = v; };
   if (n > 0) {
     if (L.bordered) {
       // chase the trailing column in (bdc.py:337-347)
-      double f = e[n - 1];
+      double f = E(n - 1);
       for (int i = n - 1; i >= 0; --i) {
         double c, s, r;
-        lartg(d[i], f, c, s, r);
-        __syncwarp();
-        d[i] = r;
+        lartg(D(i), f, c, s, r);
+        setD(i, r);
         if (i > 0) {
-          f = -s * e[i - 1];
-          e[i - 1] = c * e[i - 1];
+          const double em = E(i - 1);
+          f = -s * em;
+          setE(i - 1, c * em);
         }
         __syncwarp();
         leaf_rot(Qs, kLdQ, nc, i, n, c, s, lane);
         if (s == 0.0) break;
       }
     }
-    __syncwarp();
-    // implicit-shift QR iteration (bdc.py:273-312) on d[0..n), e[0..n-1)
+    if (lane == n - 1) er = 0.0;  // square part: e[0..n-1)
+    // implicit-shift QR iteration (bdc.py:273-312)
     double bnorm = 0.0;
-    for (int i = 0; i < n; ++i) bnorm = fmax(bnorm, fabs(d[i]));
-    for (int i = 0; i + 1 < n; ++i) bnorm = fmax(bnorm, fabs(e[i]));
+    for (int i = 0; i < n; ++i) bnorm = fmax(bnorm, fabs(D(i)));
+    for (int i = 0; i + 1 < n; ++i) bnorm = fmax(bnorm, fabs(E(i)));
     if (bnorm != 0.0) {
       const long long budget = 60LL * n * (n > 4 ? n : 4);
       long long steps = 0;
       int hi = n - 1;
       while (hi > 0) {
-        __syncwarp();
-        if (leaf_small(e[hi - 1], d[hi - 1], d[hi], bnorm)) {
-          __syncwarp();
-          e[hi - 1] = 0.0;
+        if (leaf_small(E(hi - 1), D(hi - 1), D(hi), bnorm)) {
+          setE(hi - 1, 0.0);
           --hi;
           continue;
         }
         int lo = hi - 1;
-        while (lo > 0 && !leaf_small(e[lo - 1], d[lo - 1], d[lo], bnorm)) --lo;
-        __syncwarp();
-        if (lo > 0) e[lo - 1] = 0.0;
+        while (lo > 0 && !leaf_small(E(lo - 1), D(lo - 1), D(lo), bnorm)) --lo;
+        if (lo > 0) setE(lo - 1, 0.0);
         int hit = -1;
         for (int k = lo; k <= hi; ++k)
-          if (fabs(d[k]) <= DC_EPS * bnorm * 1e-3) { hit = k; break; }
-        __syncwarp();
+          if (fabs(D(k)) <= DC_EPS * bnorm * 1e-3) { hit = k; break; }
         if (hit >= 0) {
-          d[hit] = 0.0;
+          setD(hit, 0.0);
           if (hit < hi) {
             // chase zero row (bdc.py:247-257)
-            double f = e[hit];
-            e[hit] = 0.0;
+            double f = E(hit);
+            setE(hit, 0.0);
             for (int j = hit + 1; j <= hi; ++j) {
               double c, s, r;
-              lartg(d[j], f, c, s, r);
-              __syncwarp();
-              d[j] = r;
+              lartg(D(j), f, c, s, r);
+              setD(j, r);
               if (j < hi) {
-                f = -s * e[j];
-                e[j] = c * e[j];
+                const double ej = E(j);
+                f = -s * ej;
+                setE(j, c * ej);
               }
               __syncwarp();
               leaf_rot(Ws, kLdW, n, j, hit, c, s, lane);
             }
           } else {
             // chase zero column (bdc.py:260-270)
-            double f = e[hi - 1];
-            e[hi - 1] = 0.0;
+            double f = E(hi - 1);
+            setE(hi - 1, 0.0);
             for (int j = hi - 1; j >= lo; --j) {
               double c, s, r;
-              lartg(d[j], f, c, s, r);
-              __syncwarp();
-              d[j] = r;
+              lartg(D(j), f, c, s, r);
+              setD(j, r);
               if (j > lo) {
-                f = -s * e[j - 1];
-                e[j - 1] = c * e[j - 1];
+                const double ej = E(j - 1);
+                f = -s * ej;
+                setE(j - 1, c * ej);
               }
               __syncwarp();
               leaf_rot(Qs, kLdQ, nc, j, hi, c, s, lane);
@@ -222,46 +222,43 @@ __global__ void __launch_bounds__(32 * kLeafWarps) bdc_leaf_kernel(const LeafDes
         // one bulge chase (bdc.py:218-244)
         double mu;
         {
-          const double ep = (hi - 2 >= lo) ? e[hi - 2] : 0.0;
-          const double t11 = d[hi - 1] * d[hi - 1] + ep * ep;
-          const double t12 = d[hi - 1] * e[hi - 1];
-          const double t22 = d[hi] * d[hi] + e[hi - 1] * e[hi - 1];
+          const double ep = (hi - 2 >= lo) ? E(hi - 2) : 0.0;
+          const double dh1 = D(hi - 1), eh1 = E(hi - 1), dh = D(hi);
+          const double t11 = dh1 * dh1 + ep * ep;
+          const double t12 = dh1 * eh1;
+          const double t22 = dh * dh + eh1 * eh1;
           const double delta = 0.5 * (t11 - t22);
           const double den = delta + copysign(hypot(delta, t12), delta != 0.0 ? delta : 1.0);
           mu = den == 0.0 ? t22 : t22 - t12 * t12 / den;
         }
-        double f = d[lo] * d[lo] - mu;
-        double g = d[lo] * e[lo];
+        const double dlo = D(lo);
+        double f = dlo * dlo - mu;
+        double g = dlo * E(lo);
         for (int k = lo; k < hi; ++k) {
           double c, s, r;
           lartg(f, g, c, s, r);
-          const double dk = d[k], ek = e[k], dk1 = d[k + 1];
-          __syncwarp();
-          if (k > lo) e[k - 1] = r;
+          const double dk = D(k), ek = E(k), dk1 = D(k + 1);
+          if (k > lo) setE(k - 1, r);
           f = c * dk + s * ek;
           const double ekn = c * ek - s * dk;
           g = s * dk1;
           const double dk1n = c * dk1;
-          e[k] = ekn;
-          d[k + 1] = dk1n;
+          setE(k, ekn);
           __syncwarp();
           leaf_rot(Qs, kLdQ, nc, k, k + 1, c, s, lane);
           lartg(f, g, c, s, r);
-          const double ek2 = e[k], dk1b = d[k + 1];
-          const double ekp1 = (k < hi - 1) ? e[k + 1] : 0.0;
-          __syncwarp();
-          d[k] = r;
-          f = c * ek2 + s * dk1b;
-          d[k + 1] = c * dk1b - s * ek2;
+          const double ekp1 = (k < hi - 1) ? E(k + 1) : 0.0;
+          setD(k, r);
+          f = c * ekn + s * dk1n;
+          setD(k + 1, c * dk1n - s * ekn);
           if (k < hi - 1) {
             g = s * ekp1;
-            e[k + 1] = c * ekp1;
+            setE(k + 1, c * ekp1);
           }
           __syncwarp();
           leaf_rot(Ws, kLdW, n, k, k + 1, c, s, lane);
         }
-        __syncwarp();
-        e[hi - 1] = f;
+        setE(hi - 1, f);
         steps += hi - lo;
         if (steps > budget) {
           if (lane == 0) raise_dev(err, kDevNoConvergeQR);
@@ -269,31 +266,29 @@ __global__ void __launch_bounds__(32 * kLeafWarps) bdc_leaf_kernel(const LeafDes
         }
       }
     }
-    __syncwarp();
     // sign fix into W (bdc.py:349-353)
     for (int i = 0; i < n; ++i) {
-      if (d[i] < 0.0) {
+      if (D(i) < 0.0) {
         for (int r = lane; r < n; r += 32) Ws[r + i * kLdW] = -Ws[r + i * kLdW];
       }
     }
-    __syncwarp();
-    if (lane < n) {
-      if (d[lane] < 0.0) d[lane] = -d[lane];
-    }
-    __syncwarp();
+    if (lane < n && dr < 0.0) dr = -dr;
     // stable ascending order: rank of each value
-    if (lane < n) {
-      const double x = d[lane];
+    {
       int rank = 0;
-      for (int j = 0; j < n; ++j) rank += (d[j] < x) || (d[j] == x && j < lane);
-      S.order[rank] = lane;
+      for (int j = 0; j < n; ++j) {
+        const double dj = D(j);
+        rank += (dj < dr) || (dj == dr && j < lane);
+      }
+      if (lane < n) S.order[rank] = lane;
     }
     __syncwarp();
   }
   // outputs (sorted columns)
   for (int c = 0; c < n; ++c) {
     const int src = S.order[c];
-    if (lane == 0) dv[r0 + c] = d[src];
+    const double val = D(src);
+    if (lane == 0) dv[r0 + c] = val;
     if (vectors) {
       for (int r = lane; r < n; r += 32) W[(r0 + r) + (long long)(r0 + c) * ldw] = Ws[r + src * kLdW];
       for (int r = lane; r < nc; r += 32) Q[(r0 + r) + (long long)(r0 + c) * ldq] = Qs[r + src * kLdQ];
