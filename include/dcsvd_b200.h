@@ -138,6 +138,41 @@ int dcsvd_gesdd_batched(dcsvd_handle h, int batch, int64_t m, int64_t n, double*
                         double* const* VT, int64_t ldvt, const dcsvd_opts* opts, int concurrency,
                         void* stream);
 
+/* ---- stage pieces of the reference API (single calls, device pointers) ---- */
+
+/* householder_generate (densecore.py:114-128): x[n] (stride incx), *alpha ->
+ * tau_beta[0] = tau, tau_beta[1] = beta, essential[n] = x/(alpha-beta). */
+int dcsvd_larfg(dcsvd_handle h, int64_t n, const double* alpha, const double* x, int64_t incx,
+                double* tau_beta, double* essential, void* stream);
+/* givens_generate (densecore.py:131-140) for `count` pairs: csr[3i..3i+2] = c, s, r. */
+int dcsvd_lartg(dcsvd_handle h, int64_t count, const double* a, const double* b, double* csr, void* stream);
+/* triangular_solve (densecore.py:143-171), T upper n x n: side 'L': B (n x other)
+ * <- T^-1 B (T^-T B when trans); side 'R': B (other x n) <- B T^-1 (B T^-T). */
+int dcsvd_trsm(dcsvd_handle h, char side, int trans, int64_t n, const double* T, int64_t ldt, double* B,
+               int64_t ldb, int64_t other, void* stream);
+/* build_tinv (qrblock.py:90-100): Tinv (w x w) = triu(Y^T Y, 1) + diag(1/tau), w <= 128. */
+int dcsvd_build_tinv(dcsvd_handle h, int64_t rows, int w, const double* Y, int64_t ldy, const double* tau,
+                     double* Tinv, int64_t ldt, void* stream);
+/* apply_block_reflector_left/right (qrblock.py:103-119) with a given (Y, Tinv):
+ * side 'L': C (rows_y x c_other) <- (I - Y T Y^T) C (T^T when trans);
+ * side 'R': C (c_other x rows_y) <- C (I - Y T Y^T) (T^T when trans). */
+int dcsvd_block_reflector(dcsvd_handle h, char side, int trans, int64_t rows_y, int w, const double* Y,
+                          int64_t ldy, const double* Tinv, int64_t ldt, double* C, int64_t ldc,
+                          int64_t c_other, void* stream);
+/* geqrf_panel (qrblock.py:51-71): unblocked QR of an m x w panel in place, w <= 64. */
+int dcsvd_geqrf_panel(dcsvd_handle h, int64_t m, int w, double* A, int64_t lda, double* tau, void* stream);
+/* solve_all_roots (bdc.py:515-641) of one secular system (d ascending, d[0] = 0):
+ * omega[K], anchor[K] (int32), mu[K]. */
+int dcsvd_secular_roots(dcsvd_handle h, int K, const double* d, const double* z, double* omega,
+                        int* anchor, double* mu, void* stream);
+/* recompute_z (bdc.py:644-673): Loewner update vector ztilde[K]. */
+int dcsvd_recompute_z(dcsvd_handle h, int K, const double* d, const double* z, const int* anchor,
+                      const double* mu, double* ztilde, void* stream);
+/* secular_vectors (bdc.py:676-694): U, V (K x K) column-normalised. */
+int dcsvd_secular_vectors(dcsvd_handle h, int K, const double* d, const int* anchor, const double* mu,
+                          const double* ztilde, double* U, int64_t ldu, double* V, int64_t ldv,
+                          void* stream);
+
 #ifdef __cplusplus
 }
 #endif

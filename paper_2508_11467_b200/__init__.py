@@ -23,10 +23,37 @@ from .bidiagonal import (
     gebrd_unblocked,
     labrd_panel,
 )
-from .blas import as_dense, dense_matrix, matmul_accumulate, matvec_accumulate
-from .dc import BidiagonalProblem, SubproblemSVD, bdsdc
+from .blas import (
+    GivensRotation,
+    HouseholderReflector,
+    as_dense,
+    dense_matrix,
+    givens_generate,
+    householder_generate,
+    matmul_accumulate,
+    matvec_accumulate,
+    triangular_solve,
+)
+from .dc import (
+    BidiagonalProblem,
+    SecularRoots,
+    SecularSystem,
+    SubproblemSVD,
+    bdsdc,
+    bdsqr_base,
+    recompute_z,
+    secular_vectors,
+    solve_all_roots,
+    solve_secular,
+    split,
+)
 from .householder import (
+    CompactWYBlock,
     QRFactorization,
+    apply_block_reflector_left,
+    apply_block_reflector_right,
+    build_tinv,
+    geqrf_panel,
     ReflectorSequence,
     column_reflectors,
     geqrf_blocked,
@@ -43,6 +70,24 @@ bdc = bdsdc
 __version__ = "0.1.0"
 
 __all__ = [
+    "CompactWYBlock",
+    "GivensRotation",
+    "HouseholderReflector",
+    "SecularRoots",
+    "SecularSystem",
+    "apply_block_reflector_left",
+    "apply_block_reflector_right",
+    "bdsqr_base",
+    "build_tinv",
+    "geqrf_panel",
+    "givens_generate",
+    "householder_generate",
+    "recompute_z",
+    "secular_vectors",
+    "solve_all_roots",
+    "solve_secular",
+    "split",
+    "triangular_solve",
     "BidiagonalFactorization",
     "BidiagonalProblem",
     "ConvergenceError",

@@ -22,6 +22,8 @@ EXPORTED = (
     "dcsvd_create", "dcsvd_destroy", "dcsvd_last_error", "dcsvd_version", "dcsvd_launch_count",
     "dcsvd_dgemm", "dcsvd_dgemv", "dcsvd_gebrd", "dcsvd_labrd", "dcsvd_bdsdc", "dcsvd_geqrf",
     "dcsvd_orgqr", "dcsvd_ormbr", "dcsvd_gesdd", "dcsvd_gesdd_batched", "dcsvd_set_stats", "dcsvd_get_stats",
+    "dcsvd_larfg", "dcsvd_lartg", "dcsvd_trsm", "dcsvd_build_tinv", "dcsvd_block_reflector", "dcsvd_geqrf_panel",
+    "dcsvd_secular_roots", "dcsvd_recompute_z", "dcsvd_secular_vectors",
 )
 
 
@@ -83,6 +85,15 @@ def load_library(path=None):
             "dcsvd_ormbr": (I, [V, C, I, I64, I64, V, I64, V, V, I64, I64, I64, I, V]),
             "dcsvd_gesdd": (I, [V, I64, I64, V, I64, V, V, I64, V, I64, ctypes.POINTER(DcsvdOpts),
                                 ctypes.POINTER(DcsvdPhaseTimes), V]),
+            "dcsvd_larfg": (I, [V, I64, V, V, I64, V, V, V]),
+            "dcsvd_lartg": (I, [V, I64, V, V, V, V]),
+            "dcsvd_trsm": (I, [V, C, I, I64, V, I64, V, I64, I64, V]),
+            "dcsvd_build_tinv": (I, [V, I64, I, V, I64, V, V, I64, V]),
+            "dcsvd_block_reflector": (I, [V, C, I, I64, I, V, I64, V, I64, V, I64, I64, V]),
+            "dcsvd_geqrf_panel": (I, [V, I64, I, V, I64, V, V]),
+            "dcsvd_secular_roots": (I, [V, I, V, V, V, V, V, V]),
+            "dcsvd_recompute_z": (I, [V, I, V, V, V, V, V, V]),
+            "dcsvd_secular_vectors": (I, [V, I, V, V, V, V, V, I64, V, I64, V]),
             "dcsvd_gesdd_batched": (I, [V, I, I64, I64, ctypes.POINTER(V), I64, ctypes.POINTER(V),
                                         ctypes.POINTER(V), I64, ctypes.POINTER(V), I64,
                                         ctypes.POINTER(DcsvdOpts), I, V]),

@@ -4,10 +4,93 @@ semantics of pkg/src/dcsvd/densecore.py:73-111 (``matmul_accumulate``,
 modules.  Arrays may be numpy (copied to the device and back, written in
 place like the reference) or CUDA torch tensors (computed in place)."""
 
+from dataclasses import dataclass
+
 import numpy as np
 import torch
 
 from . import _lib
+
+
+@dataclass
+class HouseholderReflector:
+    """H = I - tau y y^T, y = (1, essential) (densecore.py:33-43)."""
+
+    tau: float
+    essential: object
+    pivot_value: float
+
+
+@dataclass
+class GivensRotation:
+    """[[c, s], [-s, c]] (densecore.py:46-51)."""
+
+    c: float
+    s: float
+
+
+def householder_generate(alpha, x):
+    """Reflector mapping (alpha, x) onto (pivot, 0...), no safmin rescaling
+    (densecore.py:114-128); one GPU kernel (norm, scalars, essential)."""
+    torch_in = isinstance(x, torch.Tensor)
+    xv = _lib.vec_to_device(x).reshape(-1)
+    h = _lib.handle()
+    al = torch.tensor([float(alpha)], dtype=torch.float64, device=xv.device)
+    out = torch.empty(2, dtype=torch.float64, device=xv.device)
+    ess = torch.empty(max(xv.numel(), 1), dtype=torch.float64, device=xv.device)
+    rc = _lib.load_library().dcsvd_larfg(h, xv.numel(), _lib.ptr(al), _lib.ptr(xv), 1, _lib.ptr(out), _lib.ptr(ess),
+                                         _lib.stream_ptr())
+    _lib.check(rc, h)
+    tau, beta = (float(v) for v in out.cpu())
+    ess = ess[: xv.numel()]
+    return HouseholderReflector(tau, ess if torch_in else ess.cpu().numpy(), beta)
+
+
+def givens_generate(a, b):
+    """(GivensRotation, r) with c a + s b = r >= 0 (densecore.py:131-140)."""
+    h = _lib.handle()
+    ab = torch.tensor([float(a), float(b)], dtype=torch.float64, device="cuda")
+    out = torch.empty(3, dtype=torch.float64, device="cuda")
+    rc = _lib.load_library().dcsvd_lartg(h, 1, _lib.ptr(ab), ctypes_offset(ab, 1), _lib.ptr(out), _lib.stream_ptr())
+    _lib.check(rc, h)
+    c, s, r = (float(v) for v in out.cpu())
+    return GivensRotation(c, s), r
+
+
+def ctypes_offset(t, elems):
+    import ctypes
+
+    return ctypes.c_void_p(t.data_ptr() + 8 * elems)
+
+
+def triangular_solve(t, b, side="left", trans=False):
+    """Solve against an upper-triangular T in place on ``b``
+    (densecore.py:143-171): left B <- T^-1 B (T^-T B), right B <- B T^-1 (B T^-T).
+    Raises LinAlgError on a zero diagonal."""
+    if t.shape[0] != t.shape[1]:
+        raise ValueError(f"triangular factor must be square, got {tuple(t.shape)}")
+    n = t.shape[0]
+    if side == "left":
+        if b.shape[0] != n:
+            raise ValueError(f"shape mismatch: T is {tuple(t.shape)}, B has {b.shape[0]} rows")
+        other = b.shape[1]
+    elif side == "right":
+        if b.shape[1] != n:
+            raise ValueError(f"shape mismatch: T is {tuple(t.shape)}, B has {b.shape[1]} columns")
+        other = b.shape[0]
+    else:
+        raise ValueError(f"side must be 'left' or 'right', got {side!r}")
+    h = _lib.handle()
+    T, _ = _lib.to_device_colmajor(t, copy=False)
+    B, b_np = _lib.to_device_colmajor(b, copy=False)
+    rc = _lib.load_library().dcsvd_trsm(h, b"L" if side == "left" else b"R", int(bool(trans)), n, _lib.ptr(T), _lib.ld(T),
+                                        _lib.ptr(B), _lib.ld(B), other, _lib.stream_ptr())
+    _lib.check(rc, h)
+    if b_np:
+        b[...] = _lib.to_host(B)
+    elif B.data_ptr() != b.data_ptr():
+        b.copy_(B)
+    return b
 
 
 def _op_shape(shape, trans):

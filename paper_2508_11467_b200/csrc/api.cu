@@ -576,4 +576,75 @@ int dcsvd_gesdd_batched(dcsvd_handle h, int batch, int64_t m, int64_t n, double*
   return 0;
 }
 
+int dcsvd_larfg(dcsvd_handle h, int64_t n, const double* alpha, const double* x, int64_t incx, double* tau_beta,
+                double* essential, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  return larfg_run(h, S(stream), n, alpha, x, incx, tau_beta, essential);
+}
+
+int dcsvd_lartg(dcsvd_handle h, int64_t count, const double* a, const double* b, double* csr, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  return lartg_run(h, S(stream), count, a, b, csr);
+}
+
+int dcsvd_trsm(dcsvd_handle h, char side, int trans, int64_t n, const double* T, int64_t ldt, double* B, int64_t ldb,
+               int64_t other, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  if (side != 'L' && side != 'R') return set_error(h, DCSVD_EINVAL, "side must be 'left' or 'right'");
+  int rc = trsm_run(h, S(stream), (int)n, T, ldt, B, ldb, other, side == 'R', trans != 0);
+  if (rc) return rc;
+  return check_device_status(h, S(stream), "triangular_solve");
+}
+
+int dcsvd_build_tinv(dcsvd_handle h, int64_t rows, int w, const double* Y, int64_t ldy, const double* tau, double* Tinv,
+                     int64_t ldt, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  return build_tinv_run(h, S(stream), rows, w, Y, ldy, tau, Tinv, ldt);
+}
+
+int dcsvd_block_reflector(dcsvd_handle h, char side, int trans, int64_t rows_y, int w, const double* Y, int64_t ldy,
+                          const double* Tinv, int64_t ldt, double* C, int64_t ldc, int64_t c_other, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  if (side != 'L' && side != 'R') return set_error(h, DCSVD_EINVAL, "side must be 'L' or 'R'");
+  int rc = block_reflector_run(h, S(stream), side, trans != 0, rows_y, w, Y, ldy, Tinv, ldt, C, ldc, c_other);
+  if (rc) return rc;
+  return check_device_status(h, S(stream), "apply_block_reflector");
+}
+
+int dcsvd_geqrf_panel(dcsvd_handle h, int64_t m, int w, double* A, int64_t lda, double* tau, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  return geqr2_run(h, S(stream), m, w, A, lda, tau);
+}
+
+int dcsvd_secular_roots(dcsvd_handle h, int K, const double* d, const double* z, double* omega, int* anchor,
+                        double* mu, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  int rc = secular_run(h, S(stream), K, d, z, omega, anchor, mu);
+  if (rc) return rc;
+  return check_device_status(h, S(stream), "solve_all_roots");
+}
+
+int dcsvd_recompute_z(dcsvd_handle h, int K, const double* d, const double* z, const int* anchor, const double* mu,
+                      double* ztilde, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  int rc = loewner_run(h, S(stream), K, d, z, anchor, mu, ztilde);
+  if (rc) return rc;
+  return check_device_status(h, S(stream), "recompute_z");
+}
+
+int dcsvd_secular_vectors(dcsvd_handle h, int K, const double* d, const int* anchor, const double* mu,
+                          const double* ztilde, double* U, int64_t ldu, double* V, int64_t ldv, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  return secvec_run(h, S(stream), K, d, anchor, mu, ztilde, U, ldu, V, ldv);
+}
+
 }  // extern "C"

@@ -650,23 +650,15 @@ __global__ void bdc_rotate_kernel(const MergeDesc* __restrict__ merges, const Me
 // Secular equation: one warp per root (bdc.py:541-641).
 constexpr int kSecWarps = 8;
 
-__global__ void __launch_bounds__(32 * kSecWarps) bdc_secular_kernel(const MergeDesc* __restrict__ merges,
-                                                                     const MergeMeta* __restrict__ meta, BdcBufs B,
-                                                                     int* err) {
-  const MergeDesc M = merges[blockIdx.y];
-  const int K = meta[blockIdx.y].K;
-  const int lane = threadIdx.x & 31;
-  const int i = blockIdx.x * kSecWarps + (threadIdx.x >> 5);
-  if (i >= K) return;
-  const int r0 = M.r0;
-  const double* __restrict__ d = B.ds + r0;
-  const double* __restrict__ z = B.zs + r0;
-  const double zz = meta[blockIdx.y].zz;
+// One root of the secular equation per warp (all lanes participate; lane 0
+// stores).  d ascending with d[0] = 0, z, zz = sum z^2.
+__device__ void secular_root_warp(const double* __restrict__ d, const double* __restrict__ z, int K, double zz,
+                                  int i, int lane, double* omega, int* anc_out, double* mu_out, int* err) {
   if (K == 1) {
     if (lane == 0) {
-      B.omega[r0] = sqrt(zz);
-      B.anc[r0] = 0;
-      B.mu[r0] = zz;
+      omega[0] = sqrt(zz);
+      anc_out[0] = 0;
+      mu_out[0] = zz;
     }
     return;
   }
@@ -729,10 +721,40 @@ __global__ void __launch_bounds__(32 * kSecWarps) bdc_secular_kernel(const Merge
   }
   if (lane == 0) {
     if (!done) raise_dev(err, kDevNoConvergeSecular);
-    B.omega[r0 + i] = sqrt(fmax(da * da + mu, 0.0));
-    B.anc[r0 + i] = anc;
-    B.mu[r0 + i] = mu;
+    omega[i] = sqrt(fmax(da * da + mu, 0.0));
+    anc_out[i] = anc;
+    mu_out[i] = mu;
   }
+}
+
+__global__ void __launch_bounds__(32 * kSecWarps) bdc_secular_kernel(const MergeDesc* __restrict__ merges,
+                                                                     const MergeMeta* __restrict__ meta, BdcBufs B,
+                                                                     int* err) {
+  const MergeDesc M = merges[blockIdx.y];
+  const int K = meta[blockIdx.y].K;
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kSecWarps + (threadIdx.x >> 5);
+  if (i >= K) return;
+  const int r0 = M.r0;
+  secular_root_warp(B.ds + r0, B.zs + r0, K, meta[blockIdx.y].zz, i, lane, B.omega + r0, B.anc + r0, B.mu + r0, err);
+}
+
+// Standalone secular solve (solve_all_roots, bdc.py:515-525); zz from device.
+__global__ void __launch_bounds__(32 * kSecWarps) secular_standalone_kernel(const double* d, const double* z, int K,
+                                                                            const double* zzp, double* omega,
+                                                                            int* anc, double* mu, int* err) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kSecWarps + (threadIdx.x >> 5);
+  if (i >= K) return;
+  secular_root_warp(d, z, K, *zzp, i, lane, omega, anc, mu, err);
+}
+
+__global__ void sumsq_kernel(const double* z, int K, double* out) {
+  __shared__ double sh[32];
+  double v = 0.0;
+  for (int i = threadIdx.x; i < K; i += blockDim.x) v += z[i] * z[i];
+  v = block_sum(v, sh);
+  if (threadIdx.x == 0) *out = v;
 }
 
 // Loewner z recomputation: one warp per entry i (bdc.py:644-673).
@@ -1274,6 +1296,92 @@ int bdsdc_run(dcsvd_ctx* h, cudaStream_t st, long long n_, const double* d, cons
       note_launch();
     }
   }
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Standalone secular-equation pieces of the reference API (bdc.py:515-694),
+// on one secular system of size K held in device memory.
+
+__global__ void __launch_bounds__(32 * kSecWarps) loewner_standalone_kernel(const double* __restrict__ d,
+                                                                            const double* __restrict__ z, int K,
+                                                                            const int* __restrict__ anc,
+                                                                            const double* __restrict__ mu, double* zt,
+                                                                            int* err) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kSecWarps + (threadIdx.x >> 5);
+  if (i >= K) return;
+  const double di = d[i];
+  double prod = 1.0;
+  for (int k = lane; k < K - 1; k += 32) {
+    const double da = d[anc[k]];
+    const double num = (da - di) * (da + di) + mu[k];
+    const double dk = k < i ? d[k] : d[k + 1];
+    prod *= num / ((dk - di) * (dk + di));
+  }
+  prod = warp_prod(prod);
+  if (lane == 0) {
+    const double dl = d[anc[K - 1]];
+    const double rad = ((dl - di) * (dl + di) + mu[K - 1]) * prod;
+    if (!(rad > 0.0)) raise_dev(err, kDevInterlacing);
+    zt[i] = copysign(sqrt(rad), z[i]);
+  }
+}
+
+__global__ void __launch_bounds__(32 * kSecWarps) secvec_standalone_kernel(const double* __restrict__ d, int K,
+                                                                           const int* __restrict__ anc,
+                                                                           const double* __restrict__ mu,
+                                                                           const double* __restrict__ zt, double* U,
+                                                                           long long ldu, double* V, long long ldv) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kSecWarps + (threadIdx.x >> 5);
+  if (i >= K) return;
+  const double da = d[anc[i]], m = mu[i];
+  double sv = 0.0, su = 0.0;
+  for (int j = lane; j < K; j += 32) {
+    const double dj = d[j];
+    const double v = zt[j] / ((dj - da) * (dj + da) - m);
+    const double u = j == 0 ? -1.0 : dj * v;
+    sv += v * v;
+    su += u * u;
+  }
+  const double nv = sqrt(warp_sum(sv)), nu = sqrt(warp_sum(su));
+  for (int j = lane; j < K; j += 32) {
+    const double dj = d[j];
+    const double v = zt[j] / ((dj - da) * (dj + da) - m);
+    V[j + (long long)i * ldv] = v / nv;
+    U[j + (long long)i * ldu] = (j == 0 ? -1.0 : dj * v) / nu;
+  }
+}
+
+int secular_run(dcsvd_ctx* h, cudaStream_t st, int K, const double* d, const double* z, double* omega, int* anc,
+                double* mu) {
+  if (K < 1) return set_error(h, DCSVD_EINVAL, "secular system must be nonempty");
+  int rc = pool_reserve(h, 0, pool_bytes(1, 8), st);
+  if (rc) return rc;
+  double* zz = pool_take<double>(h, 0, 1);
+  sumsq_kernel<<<1, 256, 0, st>>>(z, K, zz);
+  secular_standalone_kernel<<<(K + kSecWarps - 1) / kSecWarps, 32 * kSecWarps, 0, st>>>(d, z, K, zz, omega, anc, mu,
+                                                                                        h->d_err);
+  note_launch(2);
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int loewner_run(dcsvd_ctx* h, cudaStream_t st, int K, const double* d, const double* z, const int* anc, const double* mu,
+                double* zt) {
+  loewner_standalone_kernel<<<(K + kSecWarps - 1) / kSecWarps, 32 * kSecWarps, 0, st>>>(d, z, K, anc, mu, zt, h->d_err);
+  note_launch();
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int secvec_run(dcsvd_ctx* h, cudaStream_t st, int K, const double* d, const int* anc, const double* mu, const double* zt,
+               double* U, long long ldu, double* V, long long ldv) {
+  secvec_standalone_kernel<<<(K + kSecWarps - 1) / kSecWarps, 32 * kSecWarps, 0, st>>>(d, K, anc, mu, zt, U, ldu, V,
+                                                                                       ldv);
+  note_launch();
   DC_CUDA_TRY(cudaGetLastError());
   return 0;
 }

@@ -82,4 +82,21 @@ int ormbr_run(dcsvd_ctx* h, cudaStream_t st, char vect, bool trans, long long m,
 int bdsdc_run(dcsvd_ctx* h, cudaStream_t st, long long n, const double* d, const double* e, bool bordered,
               bool vectors, int leaf, double tol_mult, double* dvals, double* edge_out, double* Wout,
               long long ldwo, long long wrows, double* Qout, long long ldqo, double* VT, long long ldvt);
+// standalone pieces (reference API rows)
+int build_tinv_run(dcsvd_ctx* h, cudaStream_t st, long long rows, int w, const double* Y, long long ldy,
+                   const double* tau, double* Tinv, long long ldt);
+int block_reflector_run(dcsvd_ctx* h, cudaStream_t st, char side, bool trans, long long rows_y, int w, const double* Y,
+                        long long ldy, const double* Tinv, long long ldt, double* C, long long ldc, long long c_other);
+int geqr2_run(dcsvd_ctx* h, cudaStream_t st, long long m, int w, double* A, long long lda, double* tau);
+int larfg_run(dcsvd_ctx* h, cudaStream_t st, long long n, const double* alpha, const double* x, long long incx,
+              double* out, double* ess);
+int lartg_run(dcsvd_ctx* h, cudaStream_t st, long long cnt, const double* a, const double* b, double* out);
+int trsm_run(dcsvd_ctx* h, cudaStream_t st, int n, const double* T, long long ldt, double* B, long long ldb,
+             long long other, bool right, bool trans);
+int secular_run(dcsvd_ctx* h, cudaStream_t st, int K, const double* d, const double* z, double* omega, int* anc,
+                double* mu);
+int loewner_run(dcsvd_ctx* h, cudaStream_t st, int K, const double* d, const double* z, const int* anc, const double* mu,
+                double* zt);
+int secvec_run(dcsvd_ctx* h, cudaStream_t st, int K, const double* d, const int* anc, const double* mu, const double* zt,
+               double* U, long long ldu, double* V, long long ldv);
 }  // namespace dc

@@ -132,9 +132,21 @@ static size_t cwy_scratch_doubles(int sms, long long rows_y, long long c_other, 
   return (size_t)S * (size_t)w * (size_t)c_other + (size_t)S * w * w + 2 * (size_t)w * w + 64;
 }
 
+__global__ void copy_tinv_kernel(const double* __restrict__ src, long long lds, int w, double* __restrict__ dst,
+                                 int* err) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= w * w) return;
+  const int i = idx % w, j = idx / w;
+  const double v = src[i + (long long)j * lds];
+  if (i == j && v == 0.0) raise_dev(err, kDevSingularT);
+  dst[idx] = i <= j ? v : 0.0;
+}
+
+// `utinv` (optional): caller-provided Tinv (w x w, ld ldt) instead of the one
+// built from Y and tau (apply_block_reflector_*, qrblock.py:103-119).
 static int cwy_apply(dcsvd_ctx* h, cudaStream_t st, char side, bool trans, bool ytrans, const double* Y,
                      long long ldy, const double* tau, int w, long long rows_y, double* C, long long ldc,
-                     long long c_other, double* scratch) {
+                     long long c_other, double* scratch, const double* utinv = nullptr, long long ldt = 0) {
   if (rows_y <= 0 || c_other <= 0 || w <= 0) return 0;
   // split-K so that Z's tiles x S fill the GPU
   if (w > kCwyMaxW) return set_error(h, DCSVD_EINVAL, "CWY block width %d exceeds %d", w, kCwyMaxW);
@@ -176,9 +188,13 @@ static int cwy_apply(dcsvd_ctx* h, cudaStream_t st, char side, bool trans, bool 
   if (side == 'L') rc = gemm_launch_batch(st, /*ta=*/!ytrans, /*tb=*/false, zb);
   else rc = gemm_launch_batch(st, false, /*tb=*/ytrans, zb);
   if (rc) return rc;
-  rc = gemm_launch_batch(st, !ytrans, ytrans, gb);
-  if (rc) return rc;
-  cwy_tinv_build_kernel<<<(w * w + 255) / 256, 256, 0, st>>>(Gp, S, w, tau, TinvT, h->d_err);
+  if (utinv) {
+    copy_tinv_kernel<<<(w * w + 255) / 256, 256, 0, st>>>(utinv, ldt, w, TinvT, h->d_err);
+  } else {
+    rc = gemm_launch_batch(st, !ytrans, ytrans, gb);
+    if (rc) return rc;
+    cwy_tinv_build_kernel<<<(w * w + 255) / 256, 256, 0, st>>>(Gp, S, w, tau, TinvT, h->d_err);
+  }
   cwy_tinv_solve_kernel<<<(w + 7) / 8, 256, 0, st>>>(TinvT, w, trans ? 1 : 0, Top);
   note_launch(2);
   const long long zc = (long long)w * c_other;
@@ -482,6 +498,146 @@ int ormbr_run(dcsvd_ctx* h, cudaStream_t st, char vect, bool trans, long long m,
   } else {
     return set_error(h, DCSVD_EINVAL, "vect must be 'Q' or 'P'");
   }
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Standalone pieces of the reference API (qrblock.py / densecore.py).
+
+// build_tinv (qrblock.py:90-100): Tinv = triu(Y^T Y, 1) + diag(1/tau).
+int build_tinv_run(dcsvd_ctx* h, cudaStream_t st, long long rows, int w, const double* Y, long long ldy,
+                   const double* tau, double* Tinv, long long ldt) {
+  if (w < 1 || w > kCwyMaxW) return set_error(h, DCSVD_EINVAL, "block width must be 1..%d, got %d", kCwyMaxW, w);
+  int rc = pool_reserve(h, 0, pool_bytes((size_t)2 * w * w, 8), st);
+  if (rc) return rc;
+  double* G = pool_take<double>(h, 0, (size_t)w * w);
+  double* T = pool_take<double>(h, 0, (size_t)w * w);
+  GemmDesc g;
+  g.m = w; g.n = w; g.k = (int)rows;
+  g.A = Y; g.lda = ldy; g.acol = nullptr; g.B = Y; g.ldb = ldy;
+  g.C = G; g.ldc = w; g.ccol = nullptr; g.alpha = 1.0; g.beta = 0.0;
+  if (rows > 0) {
+    rc = gemm_launch(st, true, false, g);
+    if (rc) return rc;
+  } else {
+    DC_CUDA_TRY(cudaMemsetAsync(G, 0, sizeof(double) * w * w, st));
+  }
+  cwy_tinv_build_kernel<<<(w * w + 255) / 256, 256, 0, st>>>(G, 1, w, tau, T, h->d_err);
+  note_launch();
+  DC_CUDA_TRY(cudaMemcpy2DAsync(Tinv, sizeof(double) * ldt, T, sizeof(double) * w, sizeof(double) * w, w,
+                                cudaMemcpyDeviceToDevice, st));
+  return 0;
+}
+
+// apply_block_reflector_left/right (qrblock.py:103-119) with a given (Y, Tinv).
+int block_reflector_run(dcsvd_ctx* h, cudaStream_t st, char side, bool trans, long long rows_y, int w, const double* Y,
+                        long long ldy, const double* Tinv, long long ldt, double* C, long long ldc, long long c_other) {
+  if (w < 1 || w > kCwyMaxW) return set_error(h, DCSVD_EINVAL, "block width must be 1..%d, got %d", kCwyMaxW, w);
+  const size_t need = pool_bytes(cwy_total_scratch(h->sms, rows_y, c_other, w), 8);
+  int rc = pool_reserve(h, 0, need, st);
+  if (rc) return rc;
+  double* scr = pool_take<double>(h, 0, cwy_total_scratch(h->sms, rows_y, c_other, w));
+  return cwy_apply(h, st, side, trans, false, Y, ldy, nullptr, w, rows_y, C, ldc, c_other, scr, Tinv, ldt);
+}
+
+// geqrf_panel (qrblock.py:51-71): unblocked QR of one tall panel (w <= 64).
+int geqr2_run(dcsvd_ctx* h, cudaStream_t st, long long m, int w, double* A, long long lda, double* tau) {
+  if (m < w) return set_error(h, DCSVD_EINVAL, "panel must be tall, got %lldx%d", m, w);
+  if (w < 1 || w > 64) return set_error(h, DCSVD_EINVAL, "GPU panel width must be 1..64, got %d", w);
+  int rc = pool_reserve(h, 0, pool_bytes((size_t)h->sms * 64 + 64, 8), st);
+  if (rc) return rc;
+  double* part = pool_take<double>(h, 0, (size_t)h->sms * 64 + 64);
+  return geqr2_launch(h, st, A, lda, (int)m, w, tau, part);
+}
+
+// householder_generate (densecore.py:114-128): tau, beta, essential = x/(alpha-beta).
+__global__ void larfg_kernel(int n, const double* __restrict__ alpha_p, const double* __restrict__ x, long long incx,
+                             double* __restrict__ out /* tau, beta */, double* __restrict__ ess) {
+  __shared__ double sh[32];
+  double v = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) v += x[i * incx] * x[i * incx];
+  v = block_sum(v, sh);
+  const double alpha = *alpha_p;
+  const double xn = sqrt(v);
+  double tau = 0.0, beta = alpha;
+  if (xn != 0.0) {
+    beta = -copysign(hypot(alpha, xn), alpha);
+    tau = (beta - alpha) / beta;
+  }
+  const double den = alpha - beta;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) ess[i] = xn != 0.0 ? x[i * incx] / den : x[i * incx];
+  if (threadIdx.x == 0) {
+    out[0] = tau;
+    out[1] = beta;
+  }
+}
+
+int larfg_run(dcsvd_ctx* h, cudaStream_t st, long long n, const double* alpha, const double* x, long long incx,
+              double* out, double* ess) {
+  larfg_kernel<<<1, 512, 0, st>>>((int)n, alpha, x, incx, out, ess);
+  note_launch();
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// givens_generate (densecore.py:131-140) for a batch of (a, b) pairs: out = (c, s, r).
+__global__ void lartg_kernel(long long cnt, const double* __restrict__ a, const double* __restrict__ b, double* out) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= cnt) return;
+  double c, s, r;
+  lartg(a[i], b[i], c, s, r);
+  out[3 * i + 0] = c;
+  out[3 * i + 1] = s;
+  out[3 * i + 2] = r;
+}
+
+int lartg_run(dcsvd_ctx* h, cudaStream_t st, long long cnt, const double* a, const double* b, double* out) {
+  if (cnt <= 0) return 0;
+  lartg_kernel<<<(int)((cnt + 255) / 256), 256, 0, st>>>(cnt, a, b, out);
+  note_launch();
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// triangular_solve (densecore.py:143-171), T upper n x n.  left: B <- T^-1 B
+// (or T^-T B), thread per column of B; right: B <- B T^-1 (or B T^-T), thread
+// per row of B.
+__global__ void trsm_kernel(int n, const double* __restrict__ T, long long ldt, double* __restrict__ B, long long ldb,
+                            long long other, int right, int trans, int* err) {
+  const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (v >= other) return;
+  // element stride along the solved dimension and base of this vector
+  double* x = right ? B + v : B + v * ldb;
+  const long long inc = right ? ldb : 1;
+  // left, !trans: T x = b (back substitution);  left, trans: T^T x = b (forward)
+  // right, !trans: x^T T = b^T -> T^T x = b (forward); right, trans: x^T T^T = b^T -> T x = b (back)
+  const bool upper_solve = (right != 0) == (trans != 0);
+  if (upper_solve) {
+    for (int i = n - 1; i >= 0; --i) {
+      double s = x[i * inc];
+      for (int l = i + 1; l < n; ++l) s -= T[i + l * ldt] * x[l * inc];
+      const double dg = T[i + i * ldt];
+      if (dg == 0.0) { raise_dev(err, kDevSingularT); return; }
+      x[i * inc] = s / dg;
+    }
+  } else {
+    for (int i = 0; i < n; ++i) {
+      double s = x[i * inc];
+      for (int l = 0; l < i; ++l) s -= T[l + i * ldt] * x[l * inc];
+      const double dg = T[i + i * ldt];
+      if (dg == 0.0) { raise_dev(err, kDevSingularT); return; }
+      x[i * inc] = s / dg;
+    }
+  }
+}
+
+int trsm_run(dcsvd_ctx* h, cudaStream_t st, int n, const double* T, long long ldt, double* B, long long ldb,
+             long long other, bool right, bool trans) {
+  if (other <= 0 || n <= 0) return 0;
+  trsm_kernel<<<(int)((other + 127) / 128), 128, 0, st>>>(n, T, ldt, B, ldb, other, right ? 1 : 0, trans ? 1 : 0,
+                                                          h->d_err);
+  note_launch();
   DC_CUDA_TRY(cudaGetLastError());
   return 0;
 }

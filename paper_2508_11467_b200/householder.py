@@ -127,3 +127,72 @@ def ormlq_like(seq, c, transpose=False, block=64):
     if seq.count != max(seq.packed.shape[1] - 1, 0) or seq.offset != 1:
         raise ValueError("GPU ormlq_like supports the full row-reflector sequence of a bidiagonalization")
     return _apply(seq, c, "P", transpose, block)
+
+
+@dataclass
+class CompactWYBlock:
+    """One reflector block (Y, Tinv), H_1...H_b = I - Y Tinv^-1 Y^T (qrblock.py:43-48)."""
+
+    y: object
+    tinv: object
+
+
+def build_tinv(y, tau):
+    """Tinv = strict-upper(Y^T Y) + diag(1/tau) (1 for tau == 0)
+    (qrblock.py:90-100): one DMMA GEMM + one kernel."""
+    rows, b = tuple(y.shape)
+    h = _lib.handle()
+    Y, was_np = _lib.to_device_colmajor(y, copy=False)
+    t = _lib.vec_to_device(tau, b)
+    out = _lib.colmajor_empty(b, b)
+    rc = _lib.load_library().dcsvd_build_tinv(h, rows, b, _lib.ptr(Y), _lib.ld(Y), _lib.ptr(t), _lib.ptr(out),
+                                              _lib.ld(out), _lib.stream_ptr())
+    _lib.check(rc, h)
+    return _lib.to_host(out) if was_np else out
+
+
+def _apply_block(block, c, transpose, side):
+    rows_y, b = tuple(block.y.shape)
+    h = _lib.handle()
+    Y, _ = _lib.to_device_colmajor(block.y, copy=False)
+    T, _ = _lib.to_device_colmajor(block.tinv, copy=False)
+    C, c_np = _lib.to_device_colmajor(c, copy=False)
+    other = C.shape[1] if side == "L" else C.shape[0]
+    rc = _lib.load_library().dcsvd_block_reflector(h, side.encode(), int(bool(transpose)), rows_y, b, _lib.ptr(Y),
+                                                   _lib.ld(Y), _lib.ptr(T), _lib.ld(T), _lib.ptr(C), _lib.ld(C), other,
+                                                   _lib.stream_ptr())
+    _lib.check(rc, h)
+    return _writeback(c, C, c_np)
+
+
+def apply_block_reflector_left(block, c, transpose=False):
+    """C <- (I - Y T Y^T) C, or the transposed block (qrblock.py:103-111)."""
+    if c.shape[0] != block.y.shape[0]:
+        raise ValueError(f"C has {c.shape[0]} rows, block acts on {block.y.shape[0]}")
+    return _apply_block(block, c, transpose, "L")
+
+
+def apply_block_reflector_right(block, c, transpose=False):
+    """C <- C (I - Y T Y^T), or the transposed block (qrblock.py:114-119)."""
+    if c.shape[1] != block.y.shape[0]:
+        raise ValueError(f"C has {c.shape[1]} columns, block acts on {block.y.shape[0]}")
+    return _apply_block(block, c, transpose, "R")
+
+
+def geqrf_panel(a, tau):
+    """Unblocked Householder QR of a tall panel in place (qrblock.py:51-71);
+    cooperative kernel with the panel's row slabs in shared memory."""
+    m, n = tuple(a.shape)
+    if m < n:
+        raise ValueError(f"panel must be tall, got {m}x{n}")
+    h = _lib.handle()
+    A, was_np = _lib.to_device_colmajor(a, copy=False)
+    t = torch.empty(max(n, 1), dtype=torch.float64, device=A.device)
+    rc = _lib.load_library().dcsvd_geqrf_panel(h, m, n, _lib.ptr(A), _lib.ld(A), _lib.ptr(t), _lib.stream_ptr())
+    _lib.check(rc, h)
+    _writeback(a, A, was_np)
+    if isinstance(tau, torch.Tensor):
+        tau[:n].copy_(t[:n])
+    else:
+        tau[:n] = t[:n].cpu().numpy()
+    return a

@@ -380,3 +380,136 @@ def test_gesdd_batched_high_concurrency(cuda):
         assert torch.linalg.matrix_norm(r.u.t() @ r.u - eye).item() / 2048 <= ORTH_TOL
         resid = torch.linalg.matrix_norm(a - (r.u * r.sigma) @ r.vt).item() / torch.linalg.matrix_norm(a).item()
         assert resid / 2048 <= RES_TOL
+
+
+# ---- stage pieces of the reference API (KATs from pkg/tests, oracle parity) ----
+
+def test_householder_and_givens_kats(cuda):
+    g = _g()
+    r = g.householder_generate(3.0, np.array([4.0]))      # test_densecore.py:119-123
+    assert r.pivot_value == -5.0 and abs(r.tau - 1.6) <= 1e-15
+    np.testing.assert_allclose(r.essential, [0.5], rtol=1e-15)
+    r0 = g.householder_generate(-2.0, np.zeros(3))         # zero tail: identity
+    assert r0.tau == 0.0 and r0.pivot_value == -2.0
+    rot, rr = g.givens_generate(3.0, 4.0)                  # test_densecore.py:168-172
+    np.testing.assert_allclose((rot.c, rot.s, rr), (0.6, 0.8, 5.0), rtol=1e-15)
+    rot, rr = g.givens_generate(0.0, 0.0)
+    assert (rot.c, rot.s, rr) == (1.0, 0.0, 0.0)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(300)
+    r = g.householder_generate(0.7, x)
+    tau, beta, ess = oracle.larfg(0.7, x)
+    assert abs(r.tau - tau) <= 1e-14 and abs(r.pivot_value - beta) <= 1e-13
+    assert np.max(np.abs(r.essential - ess)) <= 1e-14
+
+
+@pytest.mark.parametrize("side", ["left", "right"])
+@pytest.mark.parametrize("trans", [False, True])
+def test_triangular_solve(cuda, side, trans):
+    g = _g()
+    rng = np.random.default_rng(5)
+    t = np.triu(rng.standard_normal((40, 40))) + 5.0 * np.eye(40)
+    b = np.asfortranarray(rng.standard_normal((40, 17) if side == "left" else (17, 40)))
+    ref = b.copy()
+    g.triangular_solve(t, b, side=side, trans=trans)
+    tt = t.T if trans else t
+    back = tt @ b if side == "left" else b @ tt
+    assert np.max(np.abs(back - ref)) <= 1e-12
+    with pytest.raises(np.linalg.LinAlgError):
+        tz = t.copy()
+        tz[3, 3] = 0.0
+        g.triangular_solve(tz, b.copy(order="F"), side=side)
+
+
+def test_tinv_and_block_reflectors(cuda):
+    g = _g()
+    y = np.array([[1.0, 0.0], [1.0, 1.0], [0.0, 1.0]])    # test_qrblock.py:69-79
+    np.testing.assert_allclose(g.build_tinv(y, np.array([1.0, 2.0])), [[1.0, 1.0], [0.0, 0.5]], atol=1e-15)
+    rng = np.random.default_rng(9)
+    a = np.asfortranarray(rng.standard_normal((90, 7)))
+    tau = oracle.geqrf(a, 7)
+    y = oracle.cwy_y(a, tau)
+    tinv = g.build_tinv(y, tau)
+    np.testing.assert_allclose(tinv, oracle.cwy_tinv(y, tau), atol=1e-13)
+    blk = g.CompactWYBlock(y, tinv)
+    for trans in (False, True):
+        c = np.asfortranarray(rng.standard_normal((90, 33)))
+        c2 = c.copy(order="F")
+        g.apply_block_reflector_left(blk, c, transpose=trans)
+        oracle.cwy_apply_left(y, oracle.cwy_tinv(y, tau), c2, trans)
+        assert np.max(np.abs(c - c2)) <= 1e-13 * np.linalg.norm(c2)
+        c = np.asfortranarray(rng.standard_normal((21, 90)))
+        c2 = c.copy(order="F")
+        g.apply_block_reflector_right(blk, c, transpose=trans)
+        oracle.cwy_apply_right(y, oracle.cwy_tinv(y, tau), c2, trans)
+        assert np.max(np.abs(c - c2)) <= 1e-13 * np.linalg.norm(c2)
+
+
+def test_geqrf_panel(cuda):
+    g = _g()
+    rng = np.random.default_rng(12)
+    a = np.asfortranarray(rng.standard_normal((500, 24)))
+    a2 = a.copy(order="F")
+    tau = np.zeros(24)
+    g.geqrf_panel(a, tau)
+    tau2 = np.zeros(24)
+    oracle.geqr2(a2, tau2)
+    assert np.max(np.abs(a - a2)) <= 1e-12 * np.linalg.norm(a2)
+    assert np.max(np.abs(tau - tau2)) <= 1e-13
+
+
+def _secular_system(rng, n):
+    d = np.concatenate(([0.0], np.sort(rng.uniform(0.05, 3.0, n - 1))))
+    z = rng.standard_normal(n)
+    z[np.abs(z) < 0.02] = 0.1
+    return d, z
+
+
+def test_secular_pieces_vs_oracle(cuda):
+    g = _g()
+    # golden ratio (test_bdc.py:284-303)
+    sysg = g.SecularSystem(np.array([0.0, 1.0]), np.array([1.0, 1.0]), np.sqrt(3.0))
+    roots = g.solve_all_roots(sysg)
+    np.testing.assert_allclose(roots.omega ** 2, [(3 - np.sqrt(5)) / 2, (3 + np.sqrt(5)) / 2], rtol=1e-14)
+    zt = g.recompute_z(sysg, roots)
+    _, vmat = g.secular_vectors(sysg, roots, zt)
+    direction = np.array([-2.618034, 1.618034]) / np.linalg.norm([-2.618034, 1.618034])
+    np.testing.assert_allclose(vmat[:, 0] * np.sign(vmat[0, 0] * direction[0]), direction, rtol=1e-6)
+    rng = np.random.default_rng(51)
+    for n in (1, 2, 5, 17, 64, 300):
+        d, z = _secular_system(rng, n)
+        s = g.SecularSystem(d, z, float(np.sqrt(d[-1] ** 2 + z @ z)))
+        r = g.solve_all_roots(s)
+        om, anc, mu = oracle.secular_roots(d, z)
+        assert np.max(np.abs(r.omega - om)) <= 1e-13 * max(om.max(), 1.0)
+        for i in range(n):
+            a, m = int(r.anchor[i]), r.mu[i]
+            den = (d - d[a]) * (d + d[a]) - m
+            terms = z ** 2 / den
+            assert abs(1.0 + terms.sum()) <= 1e-12 * (1.0 + np.abs(terms).sum())
+        if n >= 3:
+            assert g.solve_secular(s, 2) == (float(r.omega[2]), int(r.anchor[2]), float(r.mu[2]))
+        zt = g.recompute_z(s, r)
+        zt2 = oracle.loewner_z(d, z, r.anchor, r.mu)
+        assert np.max(np.abs(zt - zt2)) <= 1e-12 * np.max(np.abs(zt2))
+        u, v = g.secular_vectors(s, r, zt)
+        assert np.linalg.norm(u.T @ u - np.eye(n)) <= 1e-13 * n
+        assert np.linalg.norm(v.T @ v - np.eye(n)) <= 1e-13 * n
+
+
+def test_split_and_leaf(cuda):
+    g = _g()
+    left, right, alpha, beta = g.split(g.BidiagonalProblem([1.0, 2.0, 3.0, 4.0], [5.0, 6.0, 7.0]))
+    assert left.n == 1 and left.bordered and right.n == 2 and not right.bordered and (alpha, beta) == (2.0, 6.0)
+    r = g.bdsqr_base(g.BidiagonalProblem([-3.0], np.zeros(0)))     # test_bdc.py:62-66
+    assert_array_equal(r.dvals, [3.0])
+    assert_array_equal(r.w, [[-1.0]])
+    rng = np.random.default_rng(43)
+    for bordered in (False, True):
+        p = g.BidiagonalProblem(rng.standard_normal(11), rng.standard_normal(11 if bordered else 10), bordered)
+        r = g.bdsqr_base(p)
+        o = oracle.leaf_svd(oracle.Bidiag(p.d, p.e, bordered))
+        assert np.all(np.diff(r.dvals) >= 0.0)
+        assert np.max(np.abs(r.dvals - o.vals)) <= 1e-13 * max(o.vals.max(), 1.0)
+        assert_array_equal(r.edge_rows[0], r.qfull[0, :])
+        assert_array_equal(r.edge_rows[1], r.qfull[-1, :])
