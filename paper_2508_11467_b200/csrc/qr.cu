@@ -61,16 +61,23 @@ __global__ void cwy_tinv_build_kernel(const double* __restrict__ Gp, int S, int 
 }
 
 // T = Tinv^-1, one warp per column c: right-looking back substitution with
-// the column held in registers (lane owns rows lane + 32q).  Top = T or T^T.
-__global__ void cwy_tinv_solve_kernel(const double* __restrict__ Tinv, int w, int trans, double* __restrict__ Top) {
+// the column held in registers (lane owns rows lane + 32q) and Tinv staged
+// in shared memory once per CTA.  Top = T or T^T.
+constexpr int kTinvSolveWarps = 16;
+
+__global__ void __launch_bounds__(32 * kTinvSolveWarps) cwy_tinv_solve_kernel(const double* __restrict__ Tinv, int w,
+                                                                              int trans, double* __restrict__ Top) {
+  extern __shared__ double ts[];  // w x w (ld w)
+  for (int i = threadIdx.x; i < w * w; i += blockDim.x) ts[i] = Tinv[i];
+  __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int c = blockIdx.x * kTinvSolveWarps + (threadIdx.x >> 5);
   if (c >= w) return;
   double t[kCwyMaxW / 32];
 #pragma unroll
   for (int q = 0; q < kCwyMaxW / 32; ++q) t[q] = (lane + 32 * q == c) ? 1.0 : 0.0;
   for (int i = c; i >= 0; --i) {
-    const double* col = Tinv + (long long)i * w;  // Tinv[:, i]
+    const double* col = ts + i * w;  // Tinv[:, i]
     const int qi = i >> 5, li = i & 31;
     double ti = 0.0;
 #pragma unroll
@@ -93,6 +100,20 @@ __global__ void cwy_tinv_solve_kernel(const double* __restrict__ Tinv, int w, in
       else Top[l + (long long)c * w] = v;
     }
   }
+}
+
+static int tinv_solve_launch(cudaStream_t st, const double* Tinv, int w, bool trans, double* Top) {
+  static bool attr = false;
+  if (!attr) {
+    DC_CUDA_TRY(cudaFuncSetAttribute(cwy_tinv_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kCwyMaxW * kCwyMaxW * 8));
+    attr = true;
+  }
+  cwy_tinv_solve_kernel<<<(w + kTinvSolveWarps - 1) / kTinvSolveWarps, 32 * kTinvSolveWarps, (size_t)w * w * 8, st>>>(
+      Tinv, w, trans ? 1 : 0, Top);
+  note_launch();
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
 }
 
 __global__ void splitk_reduce_kernel(double* __restrict__ Zp, long long count, int S) {
@@ -195,8 +216,9 @@ static int cwy_apply(dcsvd_ctx* h, cudaStream_t st, char side, bool trans, bool 
     if (rc) return rc;
     cwy_tinv_build_kernel<<<(w * w + 255) / 256, 256, 0, st>>>(Gp, S, w, tau, TinvT, h->d_err);
   }
-  cwy_tinv_solve_kernel<<<(w + 7) / 8, 256, 0, st>>>(TinvT, w, trans ? 1 : 0, Top);
-  note_launch(2);
+  note_launch();
+  rc = tinv_solve_launch(st, TinvT, w, trans, Top);
+  if (rc) return rc;
   const long long zc = (long long)w * c_other;
   if (S > 1) {
     splitk_reduce_kernel<<<grid_for(zc), 256, 0, st>>>(Zp, zc, S);
