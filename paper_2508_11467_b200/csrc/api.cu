@@ -18,6 +18,7 @@
 namespace dc {
 std::atomic<long long> g_launch_count{0};
 extern unsigned long long* g_labrd_tlog;
+extern bool g_labrd_last_two_phase;
 thread_local dcsvd_ctx* t_cur = nullptr;
 
 int set_error(dcsvd_ctx* h, int code, const char* fmt, ...) {
@@ -291,6 +292,9 @@ int dcsvd_debug_labrd_tlog(unsigned long long* dev_buf) {
   dc::g_labrd_tlog = dev_buf;
   return 0;
 }
+
+/* 1 when the last LABRD panel launch used the two-phase kernel (debug). */
+int dcsvd_debug_labrd_variant(void) { return dc::g_labrd_last_two_phase ? 2 : 4; }
 
 int dcsvd_create(dcsvd_handle* out, int device) {
   if (!out) return DCSVD_EINVAL;

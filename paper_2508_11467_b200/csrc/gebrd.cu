@@ -3,8 +3,13 @@
 // Reference: pkg/src/dcsvd/bidiag.py:113-204 (merged rank-2b LABRD panel +
 // single trailing GEMM), arxiv 2508.11467 Alg. 1.
 //
-// Design: one persistent cooperative kernel per panel.
-// Each column step is five phases separated by four grid barriers:
+// Design: one persistent cooperative kernel per panel, in
+// two variants chosen per panel:
+//  * labrd2_kernel (small panels, latency-bound): two phases / two grid
+//    barriers per column, the panel corrections folded into the GEMVs and the
+//    P/Q block rows/columns cached in shared memory (see the kernel comment);
+//  * labrd4_kernel (large panels, HBM-bound): each column step is five phases
+//    separated by four grid barriers, 1-D work split into per-CTA slices:
 //   P1/P5  column update  c = a[k:,k] - P[k:,:2k] Q[k,:2k]   (1-D over rows)
 //   P2     LARFG(col) + partial A^T v (2-D blocks) + partial P^T v
 //   P3     y = tau (A^T v - Q (P^T v)), row update, row norm   (1-D over cols)
@@ -16,6 +21,7 @@
 // the next one starts ("snake").  All reductions use fixed trees / fixed
 // partial order (bit-reproducible).  The trailing update A -= P Q^T is one
 // DMMA GEMM (gemm.cu).  The final <= nb columns use a single-CTA GEBD2.
+#include <algorithm>
 #include <cooperative_groups.h>
 
 #include "ctx.cuh"
@@ -35,12 +41,14 @@ struct LabrdArgs {
   double *cvec, *rvec, *normc, *normr, *py, *px, *pw, *ps;
   long long ldpy, ldpx;  // leading dims of py (>= n) and px (>= m)
   unsigned* bar;
-  int Gr, Gc, RB, CB, R1, C1;
+  int Gr, Gc, RB, CB, CBp;   // 2-D grid Gr x Gc of RB x CB blocks (CBp = CB padded)
+  int R1, C1;                // 1-D slices (labrd4_kernel)
   unsigned long long* tlog;  // optional phase timestamps (CTA 0, thread 0)
-  int cache_pq;              // P/Q 1-D slices cached in shared memory
+  int cache_pq;              // labrd4_kernel: P/Q 1-D slices cached in shared memory
 };
 
 unsigned long long* g_labrd_tlog = nullptr;  // debug: set by dcsvd_debug_labrd_tlog
+bool g_labrd_last_two_phase = false;          // debug: variant of the last launch
 
 __device__ __forceinline__ void tmark(const LabrdArgs& a, int idx) {
   if (a.tlog && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -74,6 +82,28 @@ __device__ __forceinline__ double sum_strided(const double* p, int cnt, long lon
   return s;
 }
 
+// Fixed-order sum of cnt strided partials, up to 32 loads in flight.
+__device__ __forceinline__ double sum_strided32(const double* p, int cnt, long long stride) {
+  double t[32];
+#pragma unroll
+  for (int q = 0; q < 32; ++q) t[q] = q < cnt ? p[(long long)q * stride] : 0.0;
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < 32; ++q) s += t[q];
+  for (int q = 32; q < cnt; ++q) s += p[(long long)q * stride];
+  return s;
+}
+
+// Fixed-order sum of cnt <= 160 partials, computed redundantly by every warp:
+// the same value in every thread without a block barrier.
+__device__ __forceinline__ double warp_allsum(const double* p, int cnt) {
+  const int lane = threadIdx.x & 31;
+  double t[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) t[i] = lane + 32 * i < cnt ? p[lane + 32 * i] : 0.0;
+  return warp_sum(((t[0] + t[1]) + (t[2] + t[3])) + t[4]);
+}
+
 // sum_{t < cnt} x[t * stride] * c[t] with four independent partial chains
 // (fixed combination order -> deterministic).
 __device__ __forceinline__ double dot4(const double* x, long long stride, const double* c, int cnt) {
@@ -100,12 +130,14 @@ __device__ __forceinline__ void larfg_scalars(double alpha, double nrm2, double&
   }
 }
 
-// Per-CTA caches of the panel rows of P (1-D row slice) and of Q (1-D column
+// Four-phase variant (large panels): five phases per column separated by four
+// grid barriers with the 1-D work split across CTAs in R1-row / C1-column
+// slices (see the file header).  Per-CTA caches of the panel rows of P (1-D row slice) and of Q (1-D column
 // slice): every entry of those slices is produced by this CTA (row/column
 // ownership is the same in every phase), so the per-row / per-column
 // corrections never touch global P/Q for them.
 template <int RPL>
-__global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
+__global__ void __launch_bounds__(kLabrdThreads, 1) labrd4_kernel(LabrdArgs a) {
   extern __shared__ double dsm[];
   __shared__ double sh_red[32];
   __shared__ double sh_coef[64];
@@ -424,6 +456,341 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd_kernel(LabrdArgs a) {
   }
 }
 
+
+// Two phases and two grid barriers per column.  With
+// v = [1; c/den] and u = [1; r/den_r] (LARFG, bidiag.py:136-158), the panel
+// corrections can be folded into the GEMVs on the implicitly updated matrix
+// A - P Q^T:
+//   y_j = tau (rt_j + S_j / den),  S_j = sum_{i>k} (A - P Q^T)[i,j] c_i
+//   x_i = pi  (ct_i + T_i / den_r), T_i = sum_{j>k} (A - P Q^T)[i,j] r_j
+// where ct = a[:,k] - P[:, :2k-1] Q[k, :2k-1]^T (column update before x) and
+// rt = a[k,:] - Q[:, :2k] P[k, :2k]^T (row update before y).  So:
+//   A_k  LARFG(row k-1) from the reduced row norm -> u; x_{k-1} = pi (ct + T/den_r)
+//        and c = ct - x for the block rows (O(1) per row); norm partial of c;
+//        then the local P^T c, the Q-correction of the block's partial A^T c,
+//        E = Q[:, :2k-1] P[k, :2k-1]^T for the next phase, and the partial GEMV.
+//   B_k  LARFG(col k) from the reduced norm -> v; y and r = rt - y for the
+//        block columns (O(1) per column); norm partial of r; then the local
+//        Q^T r, the P-correction of the partial A r, D = P[:, :2k] Q[k+1, :2k]^T
+//        for the next phase, and the partial GEMV.
+// Every CTA computes the 1-D quantities of its own block rows/columns
+// (identically across the other grid dimension) and keeps its P rows / Q
+// columns in shared memory; owners (gc == 0 for rows, gr == 0 for columns)
+// write them back.  Values produced in a phase are read by other CTAs only
+// after the next barrier.  Used when the P/Q block caches fit (small panels).
+template <int RPL>
+__global__ void __launch_bounds__(kLabrdThreads, 1) labrd2_kernel(LabrdArgs a) {
+  extern __shared__ double dsm[];
+  __shared__ double sh_red[32];
+  __shared__ double sh_pl[64];   // local P^T c / Q^T r (entries past the live range stay 0)
+  __shared__ double sh_row[64];  // P[k, :] (phase A) / Q[k+1, :] (phase B)
+  constexpr int RB = 32 * RPL;
+  constexpr int LP = RB + 1;     // padded leading dimension of the P cache
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = blockIdx.x, G = gridDim.x;
+  const int gr = g % a.Gr, gc = g / a.Gr;
+  const int nb = a.nb;
+  double* __restrict__ A = a.A;
+  const long long lda = a.lda, ldp = a.ldp, ldq = a.ldq;
+  double* __restrict__ P = a.P;
+  double* __restrict__ Q = a.Q;
+  unsigned epoch = 0;
+  const int br0 = gr * RB, br1 = min(a.m, br0 + RB), nbr = br1 - br0;
+  const int bc0 = gc * a.CB, bc1 = min(a.n, bc0 + a.CB), ncb = bc1 - bc0;
+  const int CBp = a.CBp, LQ = CBp + 1;
+  const bool rowowner = gc == 0, colowner = gr == 0;
+  double* sh_c = dsm;                // RB   c (rows > k) = weights of A^T c
+  double* sh_D = sh_c + RB;          // RB   P[:, :2k-2] Q[k, :2k-2]^T
+  double* sh_cp = sh_D + RB;         // RB   P-correction of A r
+  double* sh_r = sh_cp + RB;         // CBp  r (columns > k)
+  double* sh_E = sh_r + CBp;         // CBp  Q[:, :2k-1] P[k, :2k-1]^T
+  double* sh_cq = sh_E + CBp;        // CBp  Q-correction of A^T c
+  double* sh_acc = sh_cq + CBp;      // kLabrdWarps x RB
+  const int NC = (2 * nb + 3) & ~3;         // cached P/Q columns, padded to 4
+  double* Pc = sh_acc + kLabrdWarps * RB;  // LP x NC: P rows of the block
+  double* Qc = Pc + LP * NC;               // LQ x NC: Q rows of the block columns
+  {
+    const int nvec = 3 * RB + 3 * CBp;
+    const int tot = nvec + (LP + LQ) * NC;
+    for (int i = tid; i < tot; i += blockDim.x) (i < nvec ? dsm[i] : Pc[i - nvec]) = 0.0;
+    if (tid < 64) {
+      sh_pl[tid] = 0.0;
+      sh_row[tid] = 0.0;
+    }
+  }
+  __syncthreads();
+
+  for (int k = 0; k <= nb; ++k) {
+    const bool colstep = k < nb;
+    const int tb = 1 + 8 * k;
+    tmark(a, tb + 0);
+    // ======================= phase A_k (critical part: one L2 round trip of loads)
+    const int tx = 2 * k - 1;  // column of x_{k-1} (P) and u_{k-1} (Q)
+    const int rr = tid;
+    const int r = br0 + rr;
+    const bool rv = rr < nbr && r >= k;
+    double ark = 0.0, pxs = 0.0;
+    if (rv) ark = A[r + (long long)k * lda];
+    if (rv && k > 0) pxs = sum_strided32(a.px + r, a.Gc, a.ldpx);
+    double prow = 0.0;
+    if (colstep && tid < 2 * k - 1) prow = P[k + (long long)tid * ldp];  // P[k, t], t < 2k-1
+    const double yk = k > 0 ? Q[k + (long long)(2 * k - 2) * ldq] : 0.0;  // y_{k-1}[k]
+    double pi = 0.0, denr = 1.0, betar = 0.0;
+    if (k > 0) {
+      const double alr = a.rvec[k];
+      larfg_scalars(alr, warp_allsum(a.normr, a.Gc), pi, betar);
+      denr = alr - betar;
+      // u_{k-1} for the block columns j >= k; owners write Q[:, 2k-1] and row k-1 of A
+      for (int jj = tid; jj < ncb; jj += blockDim.x) {
+        const int j = bc0 + jj;
+        double u = 0.0;
+        if (j >= k) {
+          const double rj = sh_r[jj];
+          u = j == k ? 1.0 : (pi != 0.0 ? rj / denr : rj);
+          if (colowner) {
+            Q[j + (long long)tx * ldq] = u;
+            A[(k - 1) + (long long)j * lda] = j == k ? betar : u;
+          }
+        }
+        Qc[jj + tx * LQ] = u;
+      }
+      if (colowner && tid == 0 && bc0 <= k && k < bc1) {
+        a.e[k - 1] = betar;
+        a.taup[k - 1] = pi;
+      }
+    }
+    // x_{k-1} and c_k for the block rows
+    double part = 0.0;
+    if (rr < RB) {
+      double x = 0.0, c = 0.0;
+      if (rv) {
+        const double ct = ark - sh_D[rr] - (k > 0 ? Pc[rr + (2 * k - 2) * LP] * yk : 0.0);
+        if (k > 0 && pi != 0.0) x = pi * (ct + pxs / denr);
+        c = ct - x;
+        if (k > 0 && rowowner) P[r + (long long)tx * ldp] = x;
+        if (colstep) {
+          if (r == k && rowowner) a.cvec[k] = c;
+          if (r > k) part = c * c;
+        }
+      }
+      if (k > 0) Pc[rr + tx * LP] = x;
+      sh_c[rr] = (rv && r > k) ? c : 0.0;
+    }
+    if (colstep && tid < 2 * k - 1) sh_row[tid] = prow;
+    if (!colstep) break;
+    part = block_sum(part, sh_red);  // also publishes sh_c / Pc / Qc / sh_row
+    if (rowowner && tid == 0) a.normc[gr] = part;
+    tmark(a, tb + 1);
+    // local P^T c over the block rows, t < 2k (warp per t)
+    for (int t = warp; t < 2 * k; t += kLabrdWarps) {
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) s += Pc[lane + 32 * i + t * LP] * sh_c[lane + 32 * i];
+      s = warp_sum(s);
+      if (lane == 0) sh_pl[t] = s;
+    }
+    __syncthreads();
+    // Q-correction of the partial A^T c and E = Q[:, :2k-1] P[k, :2k-1]^T for
+    // the block columns j > k (thread per column, four independent chains;
+    // sh_row[2k-1] and everything past the live ranges are 0)
+    for (int jj = max(k + 1 - bc0, 0) + tid; jj < ncb; jj += blockDim.x) {
+      const double* qj = Qc + jj;
+      double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0, e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
+#pragma unroll 2
+      for (int t = 0; t < 2 * k; t += 4) {
+        const double q0 = qj[t * LQ], q1 = qj[(t + 1) * LQ], q2 = qj[(t + 2) * LQ], q3 = qj[(t + 3) * LQ];
+        c0 += q0 * sh_pl[t];
+        c1 += q1 * sh_pl[t + 1];
+        c2 += q2 * sh_pl[t + 2];
+        c3 += q3 * sh_pl[t + 3];
+        e0 += q0 * sh_row[t];
+        e1 += q1 * sh_row[t + 1];
+        e2 += q2 * sh_row[t + 2];
+        e3 += q3 * sh_row[t + 3];
+      }
+      sh_cq[jj] = (c0 + c1) + (c2 + c3);
+      sh_E[jj] = (e0 + e1) + (e2 + e3);
+    }
+    __syncthreads();
+    tmark(a, tb + 2);
+    {
+      double w[RPL];
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) w[i] = sh_c[lane + 32 * i];
+      // A^T c over the block (rows > k, columns > k), two columns per warp step
+      const int jstart = max(bc0, k + 1);
+      for (int j = jstart + warp; j < bc1; j += 2 * kLabrdWarps) {
+        const int j2 = j + kLabrdWarps;
+        const bool has2 = j2 < bc1;
+        const double* col0 = A + (long long)j * lda;
+        const double* col1 = A + (long long)(has2 ? j2 : j) * lda;
+        double x0[RPL], x1[RPL];
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) {
+          const int rw = br0 + lane + 32 * i;
+          const bool ok = rw < br1;
+          x0[i] = ok ? col0[rw] : 0.0;
+          x1[i] = ok ? col1[rw] : 0.0;
+        }
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) {
+          s0 += x0[i] * w[i];
+          s1 += x1[i] * w[i];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+          s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        }
+        if (lane == 0) {
+          a.py[(long long)gr * a.ldpy + j] = s0 - sh_cq[j - bc0];
+          if (has2) a.py[(long long)gr * a.ldpy + j2] = s1 - sh_cq[j2 - bc0];
+        }
+      }
+    }
+    tmark(a, tb + 3);
+    grid_barrier(a.bar, G, epoch);
+    tmark(a, tb + 4);
+
+    // ======================= phase B_k (critical part)
+    const int ty = 2 * k;  // column of v_k (P) and y_k (Q)
+    double akj[4], pys[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int jj = tid + q * kLabrdThreads;
+      const int j = bc0 + jj;
+      akj[q] = (jj < ncb && j > k) ? A[k + (long long)j * lda] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int jj = tid + q * kLabrdThreads;
+      const int j = bc0 + jj;
+      pys[q] = (jj < ncb && j > k) ? sum_strided32(a.py + j, a.Gr, a.ldpy) : 0.0;
+    }
+    double qrow = 0.0;
+    if (tid < 2 * k) qrow = Q[(k + 1) + (long long)tid * ldq];  // Q[k+1, t], t < 2k
+    const double xk = k > 0 ? P[k + (long long)(2 * k - 1) * ldp] : 0.0;  // x_{k-1}[k]
+    const double alpha = a.cvec[k];
+    double tau, beta;
+    larfg_scalars(alpha, warp_allsum(a.normc, a.Gr), tau, beta);
+    const double den = alpha - beta;
+    // v_k for the block rows r >= k; owners write P[:, 2k] and column k of A
+    if (rr < RB) {
+      double v = 0.0;
+      if (rv) {
+        const double cr = sh_c[rr];
+        v = r == k ? 1.0 : (tau != 0.0 ? cr / den : cr);
+        if (rowowner) {
+          P[r + (long long)ty * ldp] = v;
+          A[r + (long long)k * lda] = r == k ? beta : v;
+        }
+      }
+      Pc[rr + ty * LP] = v;
+    }
+    if (rowowner && tid == 0 && br0 <= k && k < br1) {
+      a.d[k] = beta;
+      a.tauq[k] = tau;
+    }
+    // y_k and r for the block columns j > k
+    part = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int jj = tid + q * kLabrdThreads;
+      if (jj >= ncb) break;
+      const int j = bc0 + jj;
+      double y = 0.0, rj = 0.0;
+      if (j > k) {
+        const double rt = akj[q] - sh_E[jj] - (k > 0 ? Qc[jj + (ty - 1) * LQ] * xk : 0.0);
+        if (tau != 0.0) y = tau * (rt + pys[q] / den);
+        rj = rt - y;  // P[k, 2k] = 1
+        if (colowner) {
+          Q[j + (long long)ty * ldq] = y;
+          if (j == k + 1) a.rvec[k + 1] = rj;
+        }
+        if (j > k + 1) part += rj * rj;
+      }
+      sh_r[jj] = rj;
+      Qc[jj + ty * LQ] = y;
+    }
+    if (tid < 2 * k) sh_row[tid] = qrow;
+    part = block_sum(part, sh_red);  // also publishes sh_r / Pc / Qc / sh_row
+    if (colowner && tid == 0) a.normr[gc] = part;
+    tmark(a, tb + 5);
+    const int jlo = max(bc0, k + 2);
+    // local Q^T r over the block columns (> k+1), t < 2k+1 (warp per t)
+    for (int t = warp; t < ty + 1; t += kLabrdWarps) {
+      double s = 0.0;
+#pragma unroll 4
+      for (int jj = jlo - bc0 + lane; jj < ncb; jj += 32) s += Qc[jj + t * LQ] * sh_r[jj];
+      s = warp_sum(s);
+      if (lane == 0) sh_pl[t] = s;
+    }
+    __syncthreads();
+    // P-correction of the partial A r and D = P[:, :2k] Q[k+1, :2k]^T for the
+    // block rows r > k (thread per row, four independent chains; sh_row[2k..]
+    // and sh_pl[2k+1..] are 0)
+    for (int q = max(k + 1 - br0, 0) + tid; q < nbr; q += blockDim.x) {
+      const double* pq = Pc + q;
+      double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0, d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll 2
+      for (int t = 0; t <= ty; t += 4) {
+        const double p0 = pq[t * LP], p1 = pq[(t + 1) * LP], p2 = pq[(t + 2) * LP], p3 = pq[(t + 3) * LP];
+        c0 += p0 * sh_pl[t];
+        c1 += p1 * sh_pl[t + 1];
+        c2 += p2 * sh_pl[t + 2];
+        c3 += p3 * sh_pl[t + 3];
+        d0 += p0 * sh_row[t];
+        d1 += p1 * sh_row[t + 1];
+        d2 += p2 * sh_row[t + 2];
+        d3 += p3 * sh_row[t + 3];
+      }
+      sh_cp[q] = (c0 + c1) + (c2 + c3);
+      sh_D[q] = (d0 + d1) + (d2 + d3);
+    }
+    tmark(a, tb + 6);
+    {
+      // A r over the block (rows > k, columns > k+1), descending column order
+      // (snake against the A^T c pass), two columns per warp step
+      double acc[RPL];
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) acc[i] = 0.0;
+      const int nj = bc1 - jlo;
+      for (int jj = nj - 1 - warp; jj >= 0; jj -= 2 * kLabrdWarps) {
+        const int j = jlo + jj;
+        const int jj2 = jj - kLabrdWarps;
+        const bool has2 = jj2 >= 0;
+        const int j2 = has2 ? jlo + jj2 : j;
+        const double u0 = sh_r[j - bc0];
+        const double u1 = has2 ? sh_r[j2 - bc0] : 0.0;
+        const double* col0 = A + (long long)j * lda;
+        const double* col1 = A + (long long)j2 * lda;
+        double x0[RPL], x1[RPL];
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) {
+          const int rw = br0 + lane + 32 * i;
+          const bool ok = rw < br1;
+          x0[i] = ok ? col0[rw] : 0.0;
+          x1[i] = ok ? col1[rw] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) acc[i] += x0[i] * u0 + x1[i] * u1;
+      }
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) sh_acc[warp * RB + lane + 32 * i] = acc[i];
+      __syncthreads();
+      if (rr < nbr && r > k) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < kLabrdWarps; ++w) s += sh_acc[w * RB + rr];
+        a.px[(long long)gc * a.ldpx + r] = s - sh_cp[rr];
+      }
+    }
+    tmark(a, tb + 7);
+    grid_barrier(a.bar, G, epoch);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Unblocked GEBD2 on a small trailing matrix (bidiag.py:75-110), one CTA.
 constexpr int kGebd2Threads = 1024;
@@ -516,18 +883,32 @@ __global__ void __launch_bounds__(kGebd2Threads) gebd2_kernel(double* A, long lo
 }
 
 // ---------------------------------------------------------------------------
-template <int RPL>
-static int launch_labrd(cudaStream_t st, LabrdArgs& la, int grid, size_t smem) {
-  auto kern = labrd_kernel<RPL>;
-  static bool attr = false;
-  if (!attr) {
-    DC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+constexpr int kLabrdSmemMax = 225 * 1024;  // 227 KB opt-in minus static shared memory
+
+template <typename K>
+static int launch_coop(K kern, cudaStream_t st, LabrdArgs& la, int grid, size_t smem) {
+  DC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kLabrdSmemMax));
   void* args[] = {&la};
   DC_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(kLabrdThreads), args, smem, st));
   note_launch();
   return 0;
+}
+
+static int launch_labrd(cudaStream_t st, LabrdArgs& la, int grid, size_t smem, bool two_phase, int rpl) {
+  if (two_phase) {
+    switch (rpl) {
+      case 2: return launch_coop(labrd2_kernel<2>, st, la, grid, smem);
+      case 4: return launch_coop(labrd2_kernel<4>, st, la, grid, smem);
+      case 8: return launch_coop(labrd2_kernel<8>, st, la, grid, smem);
+      default: return launch_coop(labrd2_kernel<16>, st, la, grid, smem);
+    }
+  }
+  switch (rpl) {
+    case 2: return launch_coop(labrd4_kernel<2>, st, la, grid, smem);
+    case 4: return launch_coop(labrd4_kernel<4>, st, la, grid, smem);
+    case 8: return launch_coop(labrd4_kernel<8>, st, la, grid, smem);
+    default: return launch_coop(labrd4_kernel<16>, st, la, grid, smem);
+  }
 }
 
 struct LabrdWork {
@@ -565,20 +946,6 @@ static int labrd_launch(dcsvd_ctx* h, cudaStream_t st, int mv, int nv, double* A
   DC_CUDA_TRY(cudaMemset2DAsync(P, sizeof(double) * ldp, 0, sizeof(double) * mv, 2 * nb, st));
   DC_CUDA_TRY(cudaMemset2DAsync(Q, sizeof(double) * ldq, 0, sizeof(double) * nv, 2 * nb, st));
   DC_CUDA_TRY(cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned), st));
-  // geometry: rows-per-lane by block aspect, Gr x Gc <= G
-  const double target_rows = mv / sqrt((double)G * mv / nv);
-  int rpl = 16;
-  if (target_rows <= 32 * 2) rpl = 2;
-  else if (target_rows <= 32 * 4) rpl = 4;
-  else if (target_rows <= 32 * 8) rpl = 8;
-  int RB = 32 * rpl;
-  int Gr = (mv + RB - 1) / RB;
-  if (Gr > G) return set_error(h, DCSVD_EINVAL, "matrix too tall for the GPU LABRD panel (%d rows)", mv);
-  int Gc = G / Gr;
-  if (Gc < 1) Gc = 1;
-  const int CB = (nv + Gc - 1) / Gc;
-  Gc = (nv + CB - 1) / CB;
-  const int grid = Gr * Gc;
   LabrdArgs la;
   la.A = Av; la.lda = lda; la.m = mv; la.n = nv; la.nb = nb;
   la.P = P; la.Q = Q; la.ldp = ldp; la.ldq = ldq;
@@ -586,33 +953,67 @@ static int labrd_launch(dcsvd_ctx* h, cudaStream_t st, int mv, int nv, double* A
   la.cvec = w.cvec; la.rvec = w.rvec; la.normc = w.normc; la.normr = w.normr;
   la.py = w.py; la.px = w.px; la.pw = w.pw; la.ps = w.ps; la.ldpy = w.np; la.ldpx = w.mp;
   la.bar = h->d_bar;
-  la.Gr = Gr; la.Gc = Gc; la.RB = RB; la.CB = CB;
-  la.R1 = (mv + grid - 1) / grid;
-  la.C1 = (nv + grid - 1) / grid;
   la.tlog = g_labrd_tlog;
   g_labrd_tlog = nullptr;  // log one launch only
-  if (la.R1 > kLabrdThreads || la.C1 > kLabrdThreads)
-    return set_error(h, DCSVD_EINVAL, "matrix too large for one LABRD grid (%dx%d)", mv, nv);
-  size_t smem = sizeof(double) * (((CB + 1) & ~1) + (size_t)kLabrdWarps * RB + (size_t)(la.R1 + la.C1) * 2 * nb);
-  la.cache_pq = 1;
-  if (smem > 200 * 1024) {
-    la.cache_pq = 0;
-    smem = sizeof(double) * (((CB + 1) & ~1) + (size_t)kLabrdWarps * RB);
+  // 2-D geometry for rows-per-lane rpl: Gr x Gc <= G blocks of RB x CB
+  auto geom = [&](int rpl, int& Gr, int& Gc, int& CB) {
+    const int RB = 32 * rpl;
+    Gr = (mv + RB - 1) / RB;
+    Gc = std::max(1, G / std::max(Gr, 1));
+    CB = (nv + Gc - 1) / Gc;
+    Gc = (nv + CB - 1) / CB;
+  };
+  // Two-phase kernel when its P/Q block caches fit in shared memory (small
+  // panels, latency-bound: two barriers per column); otherwise the four-phase
+  // kernel with 1-D slices (large panels, HBM-bound).
+  bool two_phase = false;
+  int rpl = 16;
+  size_t smem = 0;
+  for (int cand : {2, 4, 8, 16}) {
+    int Gr, Gc, CB;
+    geom(cand, Gr, Gc, CB);
+    if (Gr > G || CB > 4 * kLabrdThreads) continue;
+    const size_t RB = 32 * cand, CBp = (CB + 1) & ~1, NC = (2 * nb + 3) & ~3;
+    const size_t bytes = sizeof(double) * (3 * RB + 3 * CBp + (size_t)kLabrdWarps * RB + (RB + CBp + 2) * NC);
+    if (bytes <= (size_t)kLabrdSmemMax && (!two_phase || Gr * Gc > la.Gr * la.Gc)) {
+      two_phase = true;
+      rpl = cand;
+      smem = bytes;
+      la.Gr = Gr; la.Gc = Gc; la.RB = (int)RB; la.CB = CB; la.CBp = (int)CBp;
+    }
   }
-  if (smem > 200 * 1024 || CB > 4 * kLabrdThreads)
-    return set_error(h, DCSVD_EINVAL, "LABRD block too wide (%d columns)", CB);
+  if (!two_phase) {
+    const double target_rows = mv / sqrt((double)G * mv / nv);
+    rpl = 16;
+    if (target_rows <= 32 * 2) rpl = 2;
+    else if (target_rows <= 32 * 4) rpl = 4;
+    else if (target_rows <= 32 * 8) rpl = 8;
+    int Gr, Gc, CB;
+    geom(rpl, Gr, Gc, CB);
+    if (Gr > G) return set_error(h, DCSVD_EINVAL, "matrix too tall for the GPU LABRD panel (%d rows)", mv);
+    la.Gr = Gr; la.Gc = Gc; la.RB = 32 * rpl; la.CB = CB; la.CBp = (CB + 1) & ~1;
+    const int grid = Gr * Gc;
+    la.R1 = (mv + grid - 1) / grid;
+    la.C1 = (nv + grid - 1) / grid;
+    if (la.R1 > kLabrdThreads || la.C1 > kLabrdThreads)
+      return set_error(h, DCSVD_EINVAL, "matrix too large for one LABRD grid (%dx%d)", mv, nv);
+    smem = sizeof(double) * (((CB + 1) & ~1) + (size_t)kLabrdWarps * la.RB + (size_t)(la.R1 + la.C1) * 2 * nb);
+    la.cache_pq = 1;
+    if (smem > 200 * 1024) {
+      la.cache_pq = 0;
+      smem = sizeof(double) * (((CB + 1) & ~1) + (size_t)kLabrdWarps * la.RB);
+    }
+    if (smem > 200 * 1024 || CB > 4 * kLabrdThreads)
+      return set_error(h, DCSVD_EINVAL, "LABRD block too wide (%d columns)", CB);
+  }
+  const int grid = la.Gr * la.Gc;
+  g_labrd_last_two_phase = two_phase;
   // algorithmic bytes of the two big GEMVs per column:
   // 8 * sum_k [(mv-k)(nv-k-1) + (mv-k-1)(nv-k-1)]
   double bytes = 0.0;
   for (int k = 0; k < nb; ++k) bytes += 8.0 * ((double)(mv - k) * (nv - k - 1) + (double)(mv - k - 1) * (nv - k - 1));
   const int sidx = stat_begin(h, 0, bytes, st);
-  int rc;
-  switch (rpl) {
-    case 2: rc = launch_labrd<2>(st, la, grid, smem); break;
-    case 4: rc = launch_labrd<4>(st, la, grid, smem); break;
-    case 8: rc = launch_labrd<8>(st, la, grid, smem); break;
-    default: rc = launch_labrd<16>(st, la, grid, smem); break;
-  }
+  const int rc = launch_labrd(st, la, grid, smem, two_phase, rpl);
   stat_end(h, sidx, st);
   return rc;
 }
