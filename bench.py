@@ -391,7 +391,7 @@ def main():
         "accuracy": {"resid_scaled": resid, "orth_u_scaled": orth_u, "orth_v_scaled": orth_v},
         "gpu_launches": int(launches),
         "roofline": {
-            "kernel": "labrd_kernel (GEBRD panel: 2 GEMVs per column over the trailing matrix)",
+            "kernel": "labrd4_kernel + labrd2_kernel (GEBRD panels: 2 GEMVs per column over the trailing matrix)",
             "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": (achieved / hbm) if achieved else None,
             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",

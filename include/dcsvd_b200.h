@@ -173,6 +173,40 @@ int dcsvd_secular_vectors(dcsvd_handle h, int K, const double* d, const int* anc
                           const double* ztilde, double* U, int64_t ldu, double* V, int64_t ldv,
                           void* stream);
 
+/* ---- standalone merge stages of the divide and conquer (bdc.py:382-747) ---- */
+
+/* build_z (bdc.py:382-412): middle-row data of a merge in pre-sort order.
+ * left/right child values (nl / nr entries) and edge rows (2 x (n_child+1),
+ * leading dimension lde_*).  Outputs d[n], z[n] with n = nl + nr + 1 and
+ * coupling[2] = (c, s) of the bordered null-direction rotation ((1, 0) when
+ * square). */
+int dcsvd_build_z(dcsvd_handle h, int nl, int nr, int bordered, double alpha, double beta,
+                  const double* left_dvals, const double* left_edge, int64_t lde_l,
+                  const double* right_dvals, const double* right_edge, int64_t lde_r, double* d,
+                  double* z, double* coupling, void* stream);
+
+/* deflate (bdc.py:423-508): stable ascending sort of (d, z) (d[0] must be the
+ * zero border entry after sorting), tolerance tol_multiple * eps * max(|d|,|z|),
+ * z0 clamp, tiny-z and close-pair (Givens) deflation against the last kept
+ * entry.  The optional column matrices left (rows_l x n), right (rows_r x n),
+ * edge (2 x n) and int32 class arrays are permuted and rotated IN PLACE
+ * (pairs with entry 0 rotate only right/edge).  Outputs: perm[n], d_out[n],
+ * z_out[n] (sorted working copies after the rotations), kept[n], deflated[n],
+ * deflated_values[n], rot_pq[2n] (p, j pairs), rot_cs[2n] (c, s pairs) and
+ * counts[3] = {#kept, #deflated, #rotations}.  Synchronizes the stream. */
+int dcsvd_deflate(dcsvd_handle h, int n, const double* d, const double* z, double tol_multiple,
+                  double* left, int64_t rows_l, int64_t ldl, double* right, int64_t rows_r, int64_t ldr,
+                  double* edge, int64_t lde, int* left_classes, int* right_classes, int64_t* perm,
+                  double* d_out, double* z_out, int64_t* kept, int64_t* deflated,
+                  double* deflated_values, int64_t* rot_pq, double* rot_cs, int64_t* counts,
+                  void* stream);
+
+/* Gather dst[r, c] = src[row_idx ? row_idx[r] : r, col_idx ? col_idx[c] : c]
+ * (rows x cols), used by merge_vectors (bdc.py:701-747) to assemble the class
+ * blocks of its structured DMMA products (dcsvd_dgemm). */
+int dcsvd_gather(dcsvd_handle h, int64_t rows, int64_t cols, const double* src, int64_t lds,
+                 const int64_t* row_idx, const int64_t* col_idx, double* dst, int64_t ldd, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,7 +6,8 @@ Public surface mirrors pkg/src/dcsvd/__init__.py:18-129 for the hot path:
 ``PhaseProfile``, ``PHASE_NAMES``; ``gebrd_blocked`` (alias
 ``bidiagonalize``), ``labrd_panel``, ``gebrd_unblocked``,
 ``BidiagonalFactorization``, ``PanelWorkspace``; ``bdsdc`` (alias ``bdc``),
-``BidiagonalProblem``, ``SubproblemSVD``; ``geqrf_blocked``, ``orgqr``,
+``BidiagonalProblem``, ``SubproblemSVD``, ``build_z``, ``deflate``,
+``DeflationOutcome``, ``merge_vectors``; ``geqrf_blocked``, ``orgqr``,
 ``QRFactorization``; ``ormqr_like``, ``ormlq_like``, ``ReflectorSequence``,
 ``column_reflectors``, ``row_reflectors``; ``matmul_accumulate``,
 ``matvec_accumulate``; ``ConvergenceError``; plus ``gesdd_batched``.
@@ -36,6 +37,10 @@ from .blas import (
 )
 from .dc import (
     BidiagonalProblem,
+    DeflationOutcome,
+    build_z,
+    deflate,
+    merge_vectors,
     SecularRoots,
     SecularSystem,
     SubproblemSVD,
@@ -90,6 +95,10 @@ __all__ = [
     "triangular_solve",
     "BidiagonalFactorization",
     "BidiagonalProblem",
+    "DeflationOutcome",
+    "build_z",
+    "deflate",
+    "merge_vectors",
     "ConvergenceError",
     "PHASE_NAMES",
     "PanelWorkspace",

@@ -24,6 +24,7 @@ EXPORTED = (
     "dcsvd_orgqr", "dcsvd_ormbr", "dcsvd_gesdd", "dcsvd_gesdd_batched", "dcsvd_set_stats", "dcsvd_get_stats",
     "dcsvd_larfg", "dcsvd_lartg", "dcsvd_trsm", "dcsvd_build_tinv", "dcsvd_block_reflector", "dcsvd_geqrf_panel",
     "dcsvd_secular_roots", "dcsvd_recompute_z", "dcsvd_secular_vectors",
+    "dcsvd_build_z", "dcsvd_deflate", "dcsvd_gather",
 )
 
 
@@ -94,6 +95,10 @@ def load_library(path=None):
             "dcsvd_secular_roots": (I, [V, I, V, V, V, V, V, V]),
             "dcsvd_recompute_z": (I, [V, I, V, V, V, V, V, V]),
             "dcsvd_secular_vectors": (I, [V, I, V, V, V, V, V, I64, V, I64, V]),
+            "dcsvd_build_z": (I, [V, I, I, I, D, D, V, V, I64, V, V, I64, V, V, V, V]),
+            "dcsvd_deflate": (I, [V, I, V, V, D, V, I64, I64, V, I64, I64, V, I64, V, V, V, V, V, V, V, V, V, V,
+                                  V, V]),
+            "dcsvd_gather": (I, [V, I64, I64, V, I64, V, V, V, I64, V]),
             "dcsvd_gesdd_batched": (I, [V, I, I64, I64, ctypes.POINTER(V), I64, ctypes.POINTER(V),
                                         ctypes.POINTER(V), I64, ctypes.POINTER(V), I64,
                                         ctypes.POINTER(DcsvdOpts), I, V]),

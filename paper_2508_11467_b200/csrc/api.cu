@@ -19,6 +19,7 @@ namespace dc {
 std::atomic<long long> g_launch_count{0};
 extern unsigned long long* g_labrd_tlog;
 extern bool g_labrd_last_two_phase;
+extern int g_gemm_route;
 thread_local dcsvd_ctx* t_cur = nullptr;
 
 int set_error(dcsvd_ctx* h, int code, const char* fmt, ...) {
@@ -84,6 +85,8 @@ int check_device_status(dcsvd_ctx* h, cudaStream_t st, const char* stage) {
       return set_error(h, DCSVD_EARITH, "%s: root interlacing violated: non-positive radicand in z update", stage);
     case kDevSingularT:
       return set_error(h, DCSVD_ESINGULAR, "%s: triangular factor has a zero diagonal entry", stage);
+    case kDevBadDeflate:
+      return set_error(h, DCSVD_EINVAL, "%s: deflate expects one zero d entry (the border row)", stage);
     default:
       return set_error(h, DCSVD_EINVAL, "%s: device status %d", stage, code);
   }
@@ -294,6 +297,11 @@ int dcsvd_debug_labrd_tlog(unsigned long long* dev_buf) {
 }
 
 /* 1 when the last LABRD panel launch used the two-phase kernel (debug). */
+int dcsvd_debug_gemm_route(int mode) {
+  dc::g_gemm_route = mode;
+  return 0;
+}
+
 int dcsvd_debug_labrd_variant(void) { return dc::g_labrd_last_two_phase ? 2 : 4; }
 
 int dcsvd_create(dcsvd_handle* out, int device) {
@@ -652,3 +660,36 @@ int dcsvd_secular_vectors(dcsvd_handle h, int K, const double* d, const int* anc
 }
 
 }  // extern "C"
+
+int dcsvd_build_z(dcsvd_handle h, int nl, int nr, int bordered, double alpha, double beta, const double* left_dvals,
+                  const double* left_edge, int64_t lde_l, const double* right_dvals, const double* right_edge,
+                  int64_t lde_r, double* d, double* z, double* coupling, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  return build_z_run(h, S(stream), nl, nr, bordered, alpha, beta, left_dvals, left_edge, lde_l, right_dvals,
+                     right_edge, lde_r, d, z, coupling);
+}
+
+int dcsvd_deflate(dcsvd_handle h, int n, const double* d, const double* z, double tol_multiple, double* left,
+                  int64_t rows_l, int64_t ldl, double* right, int64_t rows_r, int64_t ldr, double* edge, int64_t lde,
+                  int* left_classes, int* right_classes, int64_t* perm, double* d_out, double* z_out, int64_t* kept,
+                  int64_t* deflated, double* deflated_values, int64_t* rot_pq, double* rot_cs, int64_t* counts,
+                  void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  static_assert(sizeof(long long) == sizeof(int64_t), "int64");
+  int rc = deflate_run(h, S(stream), n, d, z, tol_multiple, left, rows_l, ldl, right, rows_r, ldr, edge, lde,
+                       left_classes, right_classes, reinterpret_cast<long long*>(perm), d_out, z_out,
+                       reinterpret_cast<long long*>(kept), reinterpret_cast<long long*>(deflated), deflated_values,
+                       reinterpret_cast<long long*>(rot_pq), rot_cs, reinterpret_cast<long long*>(counts));
+  if (rc) return rc;
+  return check_device_status(h, S(stream), "deflate");
+}
+
+int dcsvd_gather(dcsvd_handle h, int64_t rows, int64_t cols, const double* src, int64_t lds, const int64_t* row_idx,
+                 const int64_t* col_idx, double* dst, int64_t ldd, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  return gather2d_run(h, S(stream), rows, cols, src, lds, reinterpret_cast<const long long*>(row_idx),
+                      reinterpret_cast<const long long*>(col_idx), dst, ldd);
+}

@@ -93,6 +93,16 @@ int larfg_run(dcsvd_ctx* h, cudaStream_t st, long long n, const double* alpha, c
 int lartg_run(dcsvd_ctx* h, cudaStream_t st, long long cnt, const double* a, const double* b, double* out);
 int trsm_run(dcsvd_ctx* h, cudaStream_t st, int n, const double* T, long long ldt, double* B, long long ldb,
              long long other, bool right, bool trans);
+int build_z_run(dcsvd_ctx* h, cudaStream_t st, int nl, int nr, int bordered, double alpha, double beta,
+                const double* ldv, const double* ledge, long long lde_l, const double* rdv, const double* redge,
+                long long lde_r, double* d, double* z, double* coupling);
+int deflate_run(dcsvd_ctx* h, cudaStream_t st, int n, const double* d_in, const double* z_in, double tol_multiple,
+                double* left, long long rows_l, long long ldl, double* right, long long rows_r, long long ldr,
+                double* edge, long long lde, int* lcls, int* rcls, long long* perm, double* d, double* z,
+                long long* kept, long long* deflated, double* dvals, long long* rot_pq, double* rot_cs,
+                long long* counts);
+int gather2d_run(dcsvd_ctx* h, cudaStream_t st, long long rows, long long cnt, const double* src, long long lds,
+                 const long long* ridx, const long long* cidx, double* dst, long long ldd);
 int secular_run(dcsvd_ctx* h, cudaStream_t st, int K, const double* d, const double* z, double* omega, int* anc,
                 double* mu);
 int loewner_run(dcsvd_ctx* h, cudaStream_t st, int K, const double* d, const double* z, const int* anc, const double* mu,

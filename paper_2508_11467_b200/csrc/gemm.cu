@@ -4,6 +4,8 @@
 
 namespace dc {
 
+int g_gemm_route = 0;  // debug: 0 default, 1 no streaming rank-k, 2 also 64x128 C-prefetch tiles
+
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   int bytes = valid ? 8 : 0;
@@ -267,6 +269,8 @@ static int launch_sized(cudaStream_t st, const GemmBatch* b, const GemmDesc* dd,
   // 64x128x16 tiles, 4 warps of 32x64, 3 stages, 2 CTAs/SM: two independent
   // CTAs per SM keep the DMMA pipe fed across each other's barriers.
   const long long tiles64x128 = (long long)((max_m + 63) / 64) * ((max_n + 127) / 128) * nz;
+  if (g_gemm_route == 2 && beta_nz)  // debug routing experiments (dcsvd_debug_gemm_route)
+    return launch_cfg<TA, TB, 64, 128, 16, 2, 2, 3, 2, true>(st, b, dd, nz, max_m, max_n);
   if (tiles64x128 >= 2 * 148 && max_k >= 128)
     return launch_cfg<TA, TB, 64, 128, 16, 2, 2, 3, 2, false>(st, b, dd, nz, max_m, max_n);
   if (beta_nz && max_k <= 64)  // rank-k updates: C read-modify-write dominates -> prefetch C
@@ -458,6 +462,7 @@ static int sm_count() {
 // Route rank-k updates (K <= 128, large M x N, plain strided operands) to the
 // streaming kernel.  Returns -1 when the shape does not qualify.
 static int try_rankk(cudaStream_t st, bool ta, bool tb, const GemmDesc& d) {
+  if (g_gemm_route != 0) return -1;
   if (ta || d.acol || d.ccol || d.k < 1 || d.k > 128 || d.beta == 0.0) return -1;
   if ((long long)d.m * d.n < (long long)1024 * 1024 || d.m < 256) return -1;
   const int sms = sm_count();

@@ -513,3 +513,156 @@ def test_split_and_leaf(cuda):
         assert np.max(np.abs(r.dvals - o.vals)) <= 1e-13 * max(o.vals.max(), 1.0)
         assert_array_equal(r.edge_rows[0], r.qfull[0, :])
         assert_array_equal(r.edge_rows[1], r.qfull[-1, :])
+
+
+# ---------------------------------------------------------------------------
+# standalone merge stages: build_z, deflate, merge_vectors (bdc.py:382-747)
+
+def test_deflate_kats(cuda):
+    g = _g()
+    out = g.deflate([0.0, 1.0, 1.0], [1.0, 0.6, 0.8])          # test_bdc.py:208-222
+    assert_array_equal(out.z, [1.0, 1.0, 0.0])
+    assert_array_equal(out.kept, [0, 1])
+    assert_array_equal(out.deflated, [2])
+    assert_array_equal(out.deflated_values, [1.0])
+    (i, j, rot), = out.applied_rotations
+    assert (i, j) == (1, 2)
+    np.testing.assert_allclose((rot.c, rot.s), (0.6, 0.8), rtol=1e-15)
+    assert_array_equal(out.system.d, [0.0, 1.0])
+    assert_array_equal(out.system.z, [1.0, 1.0])
+    out = g.deflate([0.0, 3.0, 1.0, 2.0], [1.0, 0.5, 0.5, 0.5])
+    assert_array_equal(out.d, [0.0, 1.0, 2.0, 3.0])
+    assert_array_equal(out.permutation, [0, 2, 3, 1])
+    out = g.deflate([0.0, 1.0, 2.0], [1.0, 1e-20, 1.0])        # tiny z
+    assert_array_equal(out.kept, [0, 2])
+    assert_array_equal(out.deflated, [1])
+    out = g.deflate([0.0, 1.0], [0.0, 1.0])                     # z0 clamp
+    assert 0 in out.kept and out.system.z[0] != 0.0 and abs(out.system.z[0]) <= 16.0 * np.finfo(float).eps
+    rng = np.random.default_rng(48)                              # pair with the zero entry
+    right = np.asfortranarray(rng.standard_normal((3, 3)))
+    left = np.asfortranarray(rng.standard_normal((3, 3)))
+    left0, right0 = left.copy(), right.copy()
+    out = g.deflate([0.0, 1e-18, 1.0], [0.6, 0.8, 1.0], left, right)
+    assert_array_equal(out.deflated_values, [0.0])
+    np.testing.assert_allclose(out.z[0], 1.0, rtol=1e-15)
+    assert_array_equal(left, left0)
+    assert not np.array_equal(right, right0)
+    d = np.array([0.0, 1.0, 1.0])
+    z = np.array([1.0, 0.6, 0.8])
+    g.deflate(d, z)
+    assert_array_equal(d, [0.0, 1.0, 1.0])
+    with pytest.raises(ValueError):
+        g.deflate([1.0, 2.0], [1.0, 1.0])
+
+
+def _merge_case(rng, n, clustered):
+    d = np.concatenate(([0.0], rng.uniform(0.1, 2.0, n - 1)))
+    if clustered:
+        d[1:] = np.round(d[1:] * 4) / 4                          # exact duplicates -> Givens deflation
+    z = rng.standard_normal(n)
+    z[rng.random(n) < 0.2] = 1e-19                               # tiny z -> outright deflation
+    perm = rng.permutation(n - 1) + 1
+    d[1:], z[1:] = d[perm], z[perm]
+    lcls = rng.integers(0, 4, n).astype(np.int64)
+    rcls = rng.integers(1, 4, n).astype(np.int64)
+    return d, z, lcls, rcls
+
+
+@pytest.mark.parametrize("n", [2, 7, 40, 300])
+@pytest.mark.parametrize("clustered", [False, True])
+def test_deflate_vs_oracle(cuda, n, clustered):
+    g = _g()
+    rng = np.random.default_rng(1000 + n + clustered)
+    d, z, lcls, rcls = _merge_case(rng, n, clustered)
+    L = np.asfortranarray(rng.standard_normal((n, n)))
+    R = np.asfortranarray(rng.standard_normal((n + 1, n)))
+    E = np.asfortranarray(rng.standard_normal((2, n)))
+    L2, R2, E2, lc2, rc2 = L.copy(order="F"), R.copy(order="F"), E.copy(order="F"), lcls.copy(), rcls.copy()
+    out = g.deflate(d, z, L, R, edge_rows=E, left_classes=lcls, right_classes=rcls)
+    ref = oracle.deflate_entries(d, z, L2, R2, E2, lc2, rc2)
+    assert_array_equal(out.permutation, ref["perm"])
+    assert_array_equal(out.kept, ref["kept"])
+    assert_array_equal(out.deflated, ref["deflated"])
+    assert [(i, j) for i, j, _ in out.applied_rotations] == [(p, q) for p, q, _, _ in ref["rotations"]]
+    np.testing.assert_allclose(out.deflated_values, ref["dvals"], rtol=0, atol=0)
+    np.testing.assert_allclose(out.d, ref["d"], rtol=0, atol=0)
+    np.testing.assert_allclose(out.z, ref["z"], rtol=1e-15, atol=0)
+    assert_array_equal(lcls, lc2)
+    assert_array_equal(rcls, rc2)
+    for a, b in ((L, L2), (R, R2), (E, E2)):
+        np.testing.assert_allclose(a, b, rtol=0, atol=1e-15 * np.abs(b).max())
+    assert out.system.n == ref["kept"].size
+
+
+def test_build_z_and_merge_vectors_vs_oracle(cuda):
+    g = _g()
+    rng = np.random.default_rng(45)
+    for n, bordered in ((9, False), (12, True), (40, True)):
+        prob = g.BidiagonalProblem(rng.standard_normal(n), rng.standard_normal(n if bordered else n - 1), bordered)
+        lp, rp, _, _ = g.split(prob)
+        left, right = g.bdsqr_base(lp), g.bdsqr_base(rp)
+        d, z, coupling = g.build_z(prob, left, right)
+        OL = oracle.NodeSVD(left.dvals, left.w, left.qfull, left.edge_rows)
+        OR = oracle.NodeSVD(right.dvals, right.w, right.qfull, right.edge_rows)
+        od, oz, ocp = oracle.merge_inputs(oracle.Bidiag(prob.d, prob.e, bordered), OL, OR)
+        assert_array_equal(d, od)
+        np.testing.assert_allclose(z, oz, rtol=1e-15, atol=0)
+        assert (coupling is None) == (ocp is None)
+        if bordered:
+            np.testing.assert_allclose((coupling.c, coupling.s), ocp, rtol=1e-15)
+    for rows, K, nout in ((30, 12, 12), (257, 100, 90)):
+        cols = np.asfortranarray(rng.standard_normal((rows, K + 5)))
+        cls = rng.integers(0, 4, K + 5)
+        cls[cls == 0] = 1
+        cls[3] = 0                                                # one unit column
+        kept = np.sort(rng.choice(K + 5, K, replace=False))
+        small = np.asfortranarray(rng.standard_normal((K, nout)))
+        mid = rows // 2
+        out = g.dc._structured_product(torch.from_numpy(cols).cuda(), cls, kept,
+                                       torch.from_numpy(np.ascontiguousarray(small.T)).cuda().t(), mid, mid + 1, mid)
+        ref = oracle.dc_ref._blocked_product(cols, cls, kept, small, mid, mid + 1, mid)
+        np.testing.assert_allclose(out.cpu().numpy(), ref, rtol=0, atol=1e-13 * np.abs(ref).max())
+
+
+def test_merge_from_standalone_stages(cuda):
+    """One merge assembled from build_z -> deflate -> roots -> z~ -> vectors ->
+    merge_vectors reproduces the node's singular values and vectors."""
+    g = _g()
+    rng = np.random.default_rng(49)
+    for n, bordered in ((17, False), (33, True)):
+        prob = g.BidiagonalProblem(rng.standard_normal(n), rng.standard_normal(n if bordered else n - 1), bordered)
+        lp, rp, _, _ = g.split(prob)
+        left, right = g.bdsqr_base(lp), g.bdsqr_base(rp)
+        nl, nr = left.n, right.n
+        d, z, cp = g.build_z(prob, left, right)
+        ncols = prob.ncols
+        lpre = np.zeros((n, n), order="F")
+        lpre[nl, 0] = 1.0
+        lpre[:nl, 1:1 + nl] = left.w
+        lpre[nl + 1:, 1 + nl:] = right.w
+        rpre = np.zeros((ncols, n), order="F")
+        q1 = np.zeros(ncols)
+        q1[:nl + 1] = left.qfull[:, nl]
+        if bordered:
+            q2 = np.zeros(ncols)
+            q2[nl + 1:] = right.qfull[:, nr]
+            rpre[:, 0] = cp.c * q1 + cp.s * q2
+        else:
+            rpre[:, 0] = q1
+        rpre[:nl + 1, 1:1 + nl] = left.qfull[:, :nl]
+        rpre[nl + 1:, 1 + nl:] = right.qfull[:, :nr]
+        rcls = np.full(n, 3 if bordered else 1)
+        rcls[1:1 + nl], rcls[1 + nl:] = 1, 2
+        lcls = np.zeros(n, dtype=np.int64)
+        lcls[1:1 + nl], lcls[1 + nl:] = 1, 2
+        out = g.deflate(d, z, lpre, rpre, left_classes=lcls, right_classes=rcls)
+        roots = g.solve_all_roots(out.system)
+        zt = g.recompute_z(out.system, roots)
+        umat, vmat = g.merge_vectors.__globals__["secular_vectors"](out.system, roots, zt)
+        w_cols, q_cols = g.merge_vectors(out, umat, vmat, lpre, rpre, lcls, rcls, nl)
+        vals = np.concatenate([roots.omega, out.deflated_values])
+        B = prob.dense()
+        ref = np.linalg.svd(B, compute_uv=False)
+        np.testing.assert_allclose(np.sort(vals)[::-1], ref, rtol=0, atol=1e-13 * ref[0])
+        # B q_i = sigma_i w_i for every assembled column pair
+        np.testing.assert_allclose(B @ q_cols[:, :], w_cols * vals, rtol=0, atol=1e-12 * ref[0])

@@ -71,10 +71,11 @@ def main():
                         lines.append(f"- `{k}` = {v} {u}")
                 lines.append("")
                 if "labrd" in name:
+                    key = "labrd2" if "labrd2" in name else "labrd"
                     rd = float(d["dram__bytes_read.sum"][0].replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[d["dram__bytes_read.sum"][1]]
                     wr = float(d["dram__bytes_write.sum"][0].replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[d["dram__bytes_write.sum"][1]]
-                    summ["labrd_dram_bytes_per_launch"] = rd + wr
-                    summ["labrd_capture"] = os.path.basename(a)
+                    summ[key + "_dram_bytes_per_launch"] = rd + wr
+                    summ[key + "_capture"] = os.path.basename(a)
     open(out + ".md", "w").write("\n".join(lines) + "\n")
     pj = os.path.join(os.path.dirname(out), "ncu_summary.json")
     old = json.load(open(pj)) if os.path.exists(pj) else {}
