@@ -207,6 +207,33 @@ int dcsvd_deflate(dcsvd_handle h, int n, const double* d, const double* z, doubl
 int dcsvd_gather(dcsvd_handle h, int64_t rows, int64_t cols, const double* src, int64_t lds,
                  const int64_t* row_idx, const int64_t* col_idx, double* dst, int64_t ldd, void* stream);
 
+/* ---- harness pieces on the GPU (harness.py:69-187) ---- */
+
+/* Philox-4x64-10 word stream of numpy's Philox(key=seed) (key = 128-bit seed
+ * as key_lo, key_hi): `count` outputs starting at stream word `word_offset`,
+ * written column-major into a rows x * matrix (ld).  normal = 0: uniforms
+ * ((w >> 11) + 0.5) 2^-53, bit-identical to harness._Stream.uniforms;
+ * normal = 1: Box-Muller pairs as harness._Stream.normals (consumes
+ * 2 ceil(count/2) words). */
+int dcsvd_philox(dcsvd_handle h, uint64_t key_lo, uint64_t key_hi, uint64_t word_offset, int64_t count,
+                 int normal, double* out, int64_t rows, int64_t ld, void* stream);
+
+/* prescribed_singular_values (harness.py:108-114); kind 1 logrand, 2 arith, 3 geo. */
+int dcsvd_prescribed_singular_values(dcsvd_handle h, int kind, int64_t n, double cond, uint64_t key_lo,
+                                     uint64_t key_hi, double* sigma, void* stream);
+
+/* generate_matrix (harness.py:131-146): kind 0 random (uniforms column-major),
+ * 1 logrand / 2 arith / 3 geo = U diag(sigma) V^T with Haar factors from the
+ * GPU blocked QR of Philox normals (harness.py:117-128). */
+int dcsvd_generate_matrix(dcsvd_handle h, int kind, int64_t m, int64_t n, double cond, uint64_t key_lo,
+                          uint64_t key_hi, double* A, int64_t lda, void* stream);
+
+/* accuracy (harness.py:149-187): report[4] (HOST) = {e_sigma, e_svd, orth_u,
+ * orth_v}; NaN where the reference leaves None (no ref_sigma / no U,VT). */
+int dcsvd_accuracy(dcsvd_handle h, int64_t m, int64_t n, const double* A, int64_t lda, const double* S,
+                   const double* U, int64_t ldu, const double* VT, int64_t ldvt, const double* ref_sigma,
+                   double* report, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,7 +10,10 @@ Public surface mirrors pkg/src/dcsvd/__init__.py:18-129 for the hot path:
 ``DeflationOutcome``, ``merge_vectors``; ``geqrf_blocked``, ``orgqr``,
 ``QRFactorization``; ``ormqr_like``, ``ormlq_like``, ``ReflectorSequence``,
 ``column_reflectors``, ``row_reflectors``; ``matmul_accumulate``,
-``matvec_accumulate``; ``ConvergenceError``; plus ``gesdd_batched``.
+``matvec_accumulate``; ``ConvergenceError``; the harness (``MatrixSpec``,
+``generate_matrix``, ``prescribed_singular_values``, ``accuracy``,
+``AccuracyReport``, ``read_matrix``, ``write_matrix``, ``cli_main``); plus
+``gesdd_batched``.
 
 Every numeric entry point runs hand-written sm_100a CUDA kernels from
 ``libdcsvd_b200.so`` through ctypes.  There is no CPU fallback.
@@ -67,6 +70,16 @@ from .householder import (
     ormqr_like,
     row_reflectors,
 )
+from .harness import (
+    AccuracyReport,
+    MatrixSpec,
+    accuracy,
+    cli_main,
+    generate_matrix,
+    prescribed_singular_values,
+    read_matrix,
+    write_matrix,
+)
 from .svd import PHASE_NAMES, PhaseProfile, SVDOptions, SVDResult, gesdd, gesdd_batched, phase_profile, svd
 
 bidiagonalize = gebrd_blocked
@@ -75,6 +88,14 @@ bdc = bdsdc
 __version__ = "0.1.0"
 
 __all__ = [
+    "AccuracyReport",
+    "MatrixSpec",
+    "accuracy",
+    "cli_main",
+    "generate_matrix",
+    "prescribed_singular_values",
+    "read_matrix",
+    "write_matrix",
     "CompactWYBlock",
     "GivensRotation",
     "HouseholderReflector",

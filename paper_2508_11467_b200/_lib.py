@@ -25,6 +25,7 @@ EXPORTED = (
     "dcsvd_larfg", "dcsvd_lartg", "dcsvd_trsm", "dcsvd_build_tinv", "dcsvd_block_reflector", "dcsvd_geqrf_panel",
     "dcsvd_secular_roots", "dcsvd_recompute_z", "dcsvd_secular_vectors",
     "dcsvd_build_z", "dcsvd_deflate", "dcsvd_gather",
+    "dcsvd_philox", "dcsvd_prescribed_singular_values", "dcsvd_generate_matrix", "dcsvd_accuracy",
 )
 
 
@@ -68,6 +69,7 @@ def load_library(path=None):
             )
         lib = ctypes.CDLL(p)
         V, I, I64, D, C = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_char
+        U64 = ctypes.c_uint64
         proto = {
             "dcsvd_create": (I, [ctypes.POINTER(V), I]),
             "dcsvd_destroy": (I, [V]),
@@ -99,6 +101,10 @@ def load_library(path=None):
             "dcsvd_deflate": (I, [V, I, V, V, D, V, I64, I64, V, I64, I64, V, I64, V, V, V, V, V, V, V, V, V, V,
                                   V, V]),
             "dcsvd_gather": (I, [V, I64, I64, V, I64, V, V, V, I64, V]),
+            "dcsvd_philox": (I, [V, U64, U64, U64, I64, I, V, I64, I64, V]),
+            "dcsvd_prescribed_singular_values": (I, [V, I, I64, D, U64, U64, V, V]),
+            "dcsvd_generate_matrix": (I, [V, I, I64, I64, D, U64, U64, V, I64, V]),
+            "dcsvd_accuracy": (I, [V, I64, I64, V, I64, V, V, I64, V, I64, V, ctypes.POINTER(D), V]),
             "dcsvd_gesdd_batched": (I, [V, I, I64, I64, ctypes.POINTER(V), I64, ctypes.POINTER(V),
                                         ctypes.POINTER(V), I64, ctypes.POINTER(V), I64,
                                         ctypes.POINTER(DcsvdOpts), I, V]),
@@ -194,7 +200,10 @@ def to_device_colmajor(x, copy=True):
     m, n = a.shape
     t = colmajor_empty(m, n)
     # a.T as C-contiguous == a in Fortran order; copy through a pinned staging tensor
-    host = torch.from_numpy(np.ascontiguousarray(a.T))
+    arr = np.ascontiguousarray(a.T)
+    if not arr.flags.writeable:  # e.g. read_matrix's frombuffer views
+        arr = arr.copy()
+    host = torch.from_numpy(arr)
     t.t().copy_(host, non_blocking=False)
     return t, True
 

@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libdcsvd_b200.so")
 INCLUDE = os.path.join(ROOT, "include")
-SOURCES = ["gemm.cu", "gebrd.cu", "qr.cu", "bdc.cu", "merge.cu", "api.cu"]
+SOURCES = ["gemm.cu", "gebrd.cu", "qr.cu", "bdc.cu", "merge.cu", "gen.cu", "api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]

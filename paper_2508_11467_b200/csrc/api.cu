@@ -693,3 +693,35 @@ int dcsvd_gather(dcsvd_handle h, int64_t rows, int64_t cols, const double* src, 
   return gather2d_run(h, S(stream), rows, cols, src, lds, reinterpret_cast<const long long*>(row_idx),
                       reinterpret_cast<const long long*>(col_idx), dst, ldd);
 }
+
+int dcsvd_philox(dcsvd_handle h, uint64_t key_lo, uint64_t key_hi, uint64_t word_offset, int64_t count, int normal,
+                 double* out, int64_t rows, int64_t ld, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  return philox_run(h, S(stream), key_lo, key_hi, word_offset, count, normal, out, rows, ld);
+}
+
+int dcsvd_prescribed_singular_values(dcsvd_handle h, int kind, int64_t n, double cond, uint64_t key_lo,
+                                     uint64_t key_hi, double* sigma, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  return prescribed_sigma_run(h, S(stream), kind, (int)n, cond, key_lo, key_hi, sigma);
+}
+
+int dcsvd_generate_matrix(dcsvd_handle h, int kind, int64_t m, int64_t n, double cond, uint64_t key_lo,
+                          uint64_t key_hi, double* A, int64_t lda, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  int rc = generate_run(h, S(stream), kind, m, n, cond, key_lo, key_hi, A, lda);
+  if (rc) return rc;
+  return kind == 0 ? 0 : check_device_status(h, S(stream), "generate_matrix");
+}
+
+int dcsvd_accuracy(dcsvd_handle h, int64_t m, int64_t n, const double* A, int64_t lda, const double* S_,
+                   const double* U, int64_t ldu, const double* VT, int64_t ldvt, const double* ref_sigma,
+                   double* report, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  if (m < 1 || n < 1) return set_error(h, DCSVD_EINVAL, "accuracy: empty matrix");
+  return accuracy_run(h, S(stream), m, n, A, lda, S_, U, ldu, VT, ldvt, ref_sigma, report);
+}

@@ -103,6 +103,15 @@ int deflate_run(dcsvd_ctx* h, cudaStream_t st, int n, const double* d_in, const 
                 long long* counts);
 int gather2d_run(dcsvd_ctx* h, cudaStream_t st, long long rows, long long cnt, const double* src, long long lds,
                  const long long* ridx, const long long* cidx, double* dst, long long ldd);
+int philox_run(dcsvd_ctx* h, cudaStream_t st, unsigned long long k0, unsigned long long k1, unsigned long long off,
+               long long count, int normal, double* out, long long rows, long long ld);
+int prescribed_sigma_run(dcsvd_ctx* h, cudaStream_t st, int kind, int n, double cond, unsigned long long k0,
+                         unsigned long long k1, double* sigma);
+int generate_run(dcsvd_ctx* h, cudaStream_t st, int kind, long long m, long long n, double cond, unsigned long long k0,
+                 unsigned long long k1, double* A, long long lda);
+int accuracy_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, const double* A, long long lda,
+                 const double* S, const double* U, long long ldu, const double* VT, long long ldvt,
+                 const double* ref, double* out_host);
 int secular_run(dcsvd_ctx* h, cudaStream_t st, int K, const double* d, const double* z, double* omega, int* anc,
                 double* mu);
 int loewner_run(dcsvd_ctx* h, cudaStream_t st, int K, const double* d, const double* z, const int* anc, const double* mu,

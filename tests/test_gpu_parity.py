@@ -666,3 +666,85 @@ def test_merge_from_standalone_stages(cuda):
         np.testing.assert_allclose(np.sort(vals)[::-1], ref, rtol=0, atol=1e-13 * ref[0])
         # B q_i = sigma_i w_i for every assembled column pair
         np.testing.assert_allclose(B @ q_cols[:, :], w_cols * vals, rtol=0, atol=1e-12 * ref[0])
+
+
+# ---------------------------------------------------------------------------
+# harness on the GPU: Philox stream, generators, accuracy, CLI (harness.py:69-343)
+
+def test_philox_stream_bitwise(cuda):
+    from paper_2508_11467_b200 import harness as hz
+
+    u = hz.philox_stream(0, 4).cpu().numpy()                     # test_harness.py:24-37 pin
+    assert_array_equal(u, [0.011546754286331617, 0.24154919656271817, 0.11142585551493828, 0.56441462160713374])
+    for seed in (1, 7, 2**40 + 3, 2**64 + 11):
+        for off, cnt in ((0, 1), (0, 4099), (3, 1000), (5, 17)):
+            ref = np.random.Philox(key=seed).random_raw(off + cnt)[off:]
+            ref_u = ((ref >> np.uint64(11)).astype(np.float64) + 0.5) * 2.0 ** -53
+            assert_array_equal(hz.philox_stream(seed, cnt, off).cpu().numpy(), ref_u)
+    z = hz.philox_stream(0, 2, normal=True).cpu().numpy()        # test_harness.py:39-41 pin
+    np.testing.assert_allclose(z, [0.15853383451844044, 2.9828792826170751], rtol=4e-16)
+    for seed, cnt, off in ((5, 3, 0), (11, 200001, 0), (3, 1001, 7)):
+        ref = oracle.gen_ref.WordStream(seed)
+        if off:
+            ref.uniforms(off)
+        np.testing.assert_allclose(hz.philox_stream(seed, cnt, off, normal=True).cpu().numpy(), ref.normals(cnt),
+                                   rtol=0, atol=4e-15)
+
+
+def test_generate_matrix_vs_oracle(cuda):
+    g = _g()
+    a = g.generate_matrix(g.MatrixSpec("random", 5, 3, seed=4))  # test_harness.py:73-79
+    assert a.flags.f_contiguous and a.shape == (5, 3)
+    assert_array_equal(a, oracle.make_matrix("random", 5, 3, seed=4))
+    assert_array_equal(g.generate_matrix(g.MatrixSpec("random", 300, 257, seed=2)),
+                       oracle.make_matrix("random", 300, 257, seed=2))
+    for kind, m, n, cond, seed in (("logrand", 40, 30, 1e8, 3), ("arith", 33, 33, 1e2, 1), ("geo", 20, 45, 1e10, 9),
+                                   ("logrand", 200, 130, 1e6, 0)):
+        a = g.generate_matrix(g.MatrixSpec(kind, m, n, cond, seed))
+        ref = oracle.make_matrix(kind, m, n, cond, seed)
+        assert np.max(np.abs(a - ref)) <= 1e-13
+        s = g.prescribed_singular_values(kind, min(m, n), cond, seed)
+        ref_s = oracle.gen_ref._spectrum(kind, min(m, n), cond, oracle.gen_ref.WordStream(seed))
+        np.testing.assert_allclose(s, ref_s, rtol=1e-14)
+        np.testing.assert_allclose(np.linalg.svd(a, compute_uv=False), s, rtol=0, atol=1e-13)
+
+
+def test_accuracy_report_vs_oracle(cuda):
+    g = _g()
+    a = oracle.make_matrix("random", 70, 50, seed=3)
+    r = g.gesdd(a)
+    rep = g.accuracy(a, r, reference_sigma=np.linalg.svd(a, compute_uv=False))
+    ref = oracle.accuracy_metrics(a, r.sigma, r.u, r.vt, np.linalg.svd(a, compute_uv=False))
+    for k in ("e_sigma", "e_svd", "orth_u", "orth_v"):
+        assert abs(getattr(rep, k) - ref[k]) <= 1e-15 + 1e-3 * ref[k], k
+    r0 = g.gesdd(a, g.SVDOptions(want_vectors=False))
+    rep0 = g.accuracy(a, r0)
+    assert rep0.e_sigma is None and rep0.e_svd is None and rep0.orth_u is None and rep0.orth_v is None
+    with pytest.raises(ValueError):
+        g.accuracy(a, r, reference_sigma=np.ones(3))
+
+
+def test_cli_end_to_end(cuda, tmp_path, capsys):
+    g = _g()
+    p = str(tmp_path / "a.dsvd")
+    assert g.cli_main(["gen", "--kind", "geo", "--m", "60", "--n", "40", "--cond", "1e4", "--seed", "2",
+                       "--out", p]) == 0
+    a = g.read_matrix(p)
+    assert np.max(np.abs(a - oracle.make_matrix("geo", 60, 40, 1e4, 2))) <= 1e-13
+    capsys.readouterr()
+    assert g.cli_main(["run", "--input", p, "--out-s", str(tmp_path / "s.dsvd"), "--out-u", str(tmp_path / "u.dsvd"),
+                       "--out-vt", str(tmp_path / "vt.dsvd")]) == 0
+    printed = np.array([float(x) for x in capsys.readouterr().out.split()])
+    s = g.read_matrix(str(tmp_path / "s.dsvd"))[:, 0]
+    assert_array_equal(printed, s)
+    np.testing.assert_allclose(s, g.prescribed_singular_values("geo", 40, 1e4), rtol=0, atol=1e-13)
+    u, vt = g.read_matrix(str(tmp_path / "u.dsvd")), g.read_matrix(str(tmp_path / "vt.dsvd"))
+    assert np.linalg.norm(a - (u * s) @ vt) <= 1e-13 * np.linalg.norm(a)
+    assert g.cli_main(["run", "--input", p, "--jobz", "n", "--out-u", str(tmp_path / "x")]) == 2
+    assert g.cli_main(["verify", "--input", p]) == 0
+    assert "[ok]" in capsys.readouterr().out
+    assert g.cli_main(["verify", "--input", p, "--tol", "1e-30"]) == 1
+    csv = tmp_path / "p.csv"
+    assert g.cli_main(["profile", "--input", p, "--csv", str(csv)]) == 0
+    lines = csv.read_text().splitlines()
+    assert lines[0] == "phase,seconds" and [l.split(",")[0] for l in lines[1:]] == list(g.PHASE_NAMES)
