@@ -58,8 +58,14 @@ int stat_begin(dcsvd_ctx* h, int kind, double work, cudaStream_t st) {
   dcsvd_ctx::StatRec r;
   r.kind = kind;
   r.work = work;
-  cudaEventCreate(&r.a);
-  cudaEventCreate(&r.b);
+  for (cudaEvent_t* e : {&r.a, &r.b}) {
+    if (!h->ev_free.empty()) {
+      *e = h->ev_free.back();
+      h->ev_free.pop_back();
+    } else {
+      cudaEventCreate(e);
+    }
+  }
   cudaEventRecord(r.a, st);
   h->stats.push_back(r);
   return (int)h->stats.size() - 1;
@@ -297,6 +303,9 @@ int dcsvd_debug_labrd_tlog(unsigned long long* dev_buf) {
 }
 
 /* 1 when the last LABRD panel launch used the two-phase kernel (debug). */
+/* number of concurrent batch sub-contexts (streams) of a handle (debug) */
+int dcsvd_debug_batch_streams(dcsvd_handle h) { return h ? (int)h->subs.size() : 0; }
+
 int dcsvd_debug_gemm_route(int mode) {
   dc::g_gemm_route = mode;
   return 0;
@@ -348,11 +357,12 @@ int dcsvd_set_stats(dcsvd_handle h, int enable) {
   cudaSetDevice(h->device);
   cudaDeviceSynchronize();
   for (auto& r : h->stats) {
-    cudaEventDestroy(r.a);
-    cudaEventDestroy(r.b);
+    h->ev_free.push_back(r.a);
+    h->ev_free.push_back(r.b);
   }
   h->stats.clear();
   h->stats_on = enable != 0;
+  for (auto* sub : h->subs) dcsvd_set_stats(sub, enable);  // batched sub-contexts record too
   return 0;
 }
 
@@ -387,6 +397,14 @@ int dcsvd_get_stats(dcsvd_handle h, int kind, double* ms, double* work, long lon
     if (cudaEventElapsedTime(&x, r.a, r.b) == cudaSuccess) t += x;
     w += r.work;
     ++c;
+  }
+  for (auto* sub : h->subs) {  // batched sub-contexts (concurrent streams: times add up per stream)
+    double st = 0.0, sw = 0.0;
+    long long sc = 0;
+    dcsvd_get_stats(sub, kind, &st, &sw, &sc);
+    t += st;
+    w += sw;
+    c += sc;
   }
   if (ms) *ms = t;
   if (work) *work = w;

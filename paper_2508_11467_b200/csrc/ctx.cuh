@@ -33,6 +33,7 @@ struct dcsvd_ctx {
     double work;
   };
   std::vector<StatRec> stats;
+  std::vector<cudaEvent_t> ev_free;  // recycled timing events (no create/destroy per launch)
 };
 
 namespace dc {

@@ -1,8 +1,11 @@
 // DMMA GEMM kernels (see gemm.cuh).
+#include "ctx.cuh"
 #include "gemm.cuh"
 #include "launch.cuh"
 
 namespace dc {
+
+extern thread_local dcsvd_ctx* t_cur;  // api.cu: handle of the current API call
 
 int g_gemm_route = 0;  // debug: 0 default, 1 no streaming rank-k, 2 also 64x128 C-prefetch tiles
 
@@ -481,24 +484,34 @@ static int dispatch(cudaStream_t st, bool ta, bool tb, const GemmBatch* b, const
 
 int gemm_launch(cudaStream_t st, bool ta, bool tb, const GemmDesc& d) {
   if (d.m <= 0 || d.n <= 0) return 0;
-  const int r = try_rankk(st, ta, tb, d);
-  if (r >= 0) return r;
-  GemmBatch b;
-  b.d[0] = d;
-  b.count = 1;
-  return dispatch(st, ta, tb, &b, nullptr, 1, d.m, d.n, d.k, d.beta != 0.0);
+  // kernel-family timing (dcsvd_set_stats, kind 1 = DMMA GEMM flops)
+  const int sidx = t_cur ? stat_begin(t_cur, 1, 2.0 * d.m * d.n * d.k, st) : -1;
+  int r = try_rankk(st, ta, tb, d);
+  if (r < 0) {
+    GemmBatch b;
+    b.d[0] = d;
+    b.count = 1;
+    r = dispatch(st, ta, tb, &b, nullptr, 1, d.m, d.n, d.k, d.beta != 0.0);
+  }
+  if (t_cur) stat_end(t_cur, sidx, st);
+  return r;
 }
 
 int gemm_launch_batch(cudaStream_t st, bool ta, bool tb, const GemmBatch& b) {
   int mm = 0, nn = 0, kk = 0;
   bool bnz = false;
+  double flops = 0.0;
   for (int i = 0; i < b.count; ++i) {
     bnz = bnz || b.d[i].beta != 0.0;
     mm = b.d[i].m > mm ? b.d[i].m : mm;
     nn = b.d[i].n > nn ? b.d[i].n : nn;
     kk = b.d[i].k > kk ? b.d[i].k : kk;
+    flops += 2.0 * b.d[i].m * b.d[i].n * b.d[i].k;
   }
-  return dispatch(st, ta, tb, &b, nullptr, b.count, mm, nn, kk, bnz);
+  const int sidx = t_cur ? stat_begin(t_cur, 1, flops, st) : -1;
+  const int r = dispatch(st, ta, tb, &b, nullptr, b.count, mm, nn, kk, bnz);
+  if (t_cur) stat_end(t_cur, sidx, st);
+  return r;
 }
 
 int gemm_launch_device(cudaStream_t st, bool ta, bool tb, const GemmDesc* ddesc, int ndesc, int max_m,
