@@ -57,6 +57,14 @@ __device__ __forceinline__ void tmark(const LabrdArgs& a, int idx) {
     a.tlog[idx] = t;
   }
 }
+// debug: per-CTA timestamp (slot base + CTA) for one column step (skew analysis, tools/labrd_skew.py)
+__device__ __forceinline__ void tmark_cta(const LabrdArgs& a, int k, int base) {
+  if (a.tlog && k == 5 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.tlog[base + blockIdx.x] = t;
+  }
+}
 
 constexpr int kLabrdThreads = 512;
 constexpr int kLabrdWarps = kLabrdThreads / 32;
@@ -280,9 +288,11 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd4_kernel(LabrdArgs a) {
         if (lane == 0) a.pw[gr * 64 + t] = s;
       }
     }
+    tmark_cta(a, k, 400);
     tmark(a, tb + 2);
     grid_barrier(a.bar, G, epoch);
     tmark(a, tb + 3);
+    tmark_cta(a, k, 600);
 
     // ================= phase 3: y, row update, row norm partial
     double pys = 0.0, akj = 0.0;
@@ -406,9 +416,11 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd4_kernel(LabrdArgs a) {
         if (lane == 0) a.ps[gc * 64 + t] = s;
       }
     }
+    tmark_cta(a, k, 800);
     tmark(a, tb + 7);
     grid_barrier(a.bar, G, epoch);
     tmark(a, tb + 8);
+    tmark_cta(a, k, 1000);
 
     // ================= phase 5: x, next column update
     const bool next = k + 1 < nb;
