@@ -124,3 +124,44 @@ def test_batch_gather_two_ranks_gloo():
         p.join(timeout=120)
         assert p.exitcode == 0
     assert order == [float(i) for i in range(10)]
+
+
+# the `dcsvd` shim: reference module layout -> this package
+REFERENCE_ALL = (  # pkg/src/dcsvd/__init__.py:87-129
+    "AccuracyReport BidiagonalFactorization BidiagonalProblem CompactWYBlock ConvergenceError DeflationOutcome "
+    "GivensRotation HouseholderReflector MatrixSpec PhaseProfile QRFactorization ReflectorSequence SVDOptions "
+    "SVDResult SecularRoots SecularSystem SubproblemSVD accuracy apply_block_reflector_left "
+    "apply_block_reflector_right as_dense bdsdc bdsqr_base build_tinv build_z cli_main column_reflectors deflate "
+    "dense_matrix gebrd_blocked gebrd_unblocked generate_matrix geqrf_blocked geqrf_panel gesdd givens_generate "
+    "householder_generate labrd_panel matmul_accumulate matvec_accumulate merge_vectors orgqr ormlq_like ormqr_like "
+    "phase_profile prescribed_singular_values read_matrix recompute_z row_reflectors secular_vectors "
+    "solve_all_roots solve_secular split triangular_solve write_matrix").split()
+
+
+def test_dcsvd_shim_layout():
+    import importlib
+    import os
+    import sys
+
+    shim = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "shim")
+    sys.path.insert(0, shim)
+    try:
+        d = importlib.import_module("dcsvd")
+        for name in REFERENCE_ALL:
+            assert hasattr(d, name), name
+        for mod, names in (("driver", "gesdd phase_profile SVDOptions SVDResult PhaseProfile PHASE_NAMES"),
+                           ("bdc", "bdsdc deflate build_z merge_vectors split bdsqr_base"),
+                           ("bidiag", "gebrd_blocked labrd_panel gebrd_unblocked"),
+                           ("qrblock", "geqrf_blocked orgqr build_tinv"),
+                           ("backtransform", "ormqr_like ormlq_like column_reflectors row_reflectors"),
+                           ("densecore", "matmul_accumulate householder_generate ConvergenceError"),
+                           ("harness", "MatrixSpec generate_matrix accuracy read_matrix write_matrix cli_main")):
+            m = importlib.import_module("dcsvd." + mod)
+            for name in names.split():
+                assert hasattr(m, name), (mod, name)
+        import paper_2508_11467_b200 as g
+        assert d.gesdd is g.gesdd and d.bdc.deflate is g.deflate
+    finally:
+        sys.path.remove(shim)
+        for k in [k for k in sys.modules if k == "dcsvd" or k.startswith("dcsvd.")]:
+            del sys.modules[k]
