@@ -330,8 +330,11 @@ __global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P) {
 
   auto load_a = [&](int buf, int m0) {
     double* as = As + buf * Cfg::A_ELEMS;
-    for (int p = tid; p < MT * Kp / 2; p += THREADS) {  // A: [k][m], pairs along m
+#pragma unroll
+    for (int p0 = 0; p0 < MT * KMAX / 2; p0 += THREADS) {  // A: [k][m], pairs along m (compile-time trip count)
+      const int p = p0 + tid;
       const int i = 2 * (p % (MT / 2)), kk = p / (MT / 2);
+      if (kk >= Kp) break;
       const int gm = m0 + i;
       const int valid = kk < K ? max(0, min(2, M - gm)) : 0;
       const double* src = valid ? A + (long long)gm + (long long)kk * lda : A;
