@@ -106,6 +106,10 @@ int dc_cuda_fail(cudaError_t e, const char* what) {
 
 using namespace dc;
 
+extern "C" {
+static dcsvd_ctx* make_sub(dcsvd_ctx* h, int sms);
+}
+
 namespace {
 struct Guard {
   Guard(dcsvd_ctx* h) {
@@ -182,6 +186,26 @@ struct PhaseTimer {
     }
   }
 };
+// device status of a side/sub context folded into the parent's (stream-ordered)
+__global__ void merge_err_kernel(int* dst, int* src) {
+  if (*src != 0 && *dst == 0) *dst = *src;
+  *src = 0;
+}
+
+// Lazily created side context (whole-GPU handles only; batch sub-contexts
+// already share the GPU).
+static dcsvd_ctx* side_ctx(dcsvd_ctx* h) {
+  if (h->is_sub) return nullptr;
+  if (!h->side) {
+    h->side = make_sub(h, h->sms);
+    if (!h->side) return nullptr;
+    if (cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess)
+      return nullptr;
+  }
+  h->side->stats_on = h->stats_on;
+  return h->side;
+}
 constexpr int kDriverCwyWidth = 128;
 enum { PH_GEQRF = 0, PH_ORGQR, PH_GEBRD, PH_BDC, PH_ORMBR, PH_GEMM, PH_END = -1 };
 
@@ -207,9 +231,27 @@ int square_core(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double*
   // take (kDriverCwyWidth): T^-1 = triu(Y^T Y) + diag(1/tau) is exact for any
   // width, so this is the same product as the reference's 64-wide blocks
   // (backtransform.py:90-131) with fewer, larger DMMA GEMMs.
+  // The U and V^T back-transforms are independent: on a whole-GPU handle the
+  // V^T one runs on a side stream with its own workspace, so the small
+  // kernels and wave tails of one fill the other's gaps.
+  dcsvd_ctx* sd = side_ctx(h);
+  if (!sd) {
+    rc = ormbr_run(h, st, 'Q', false, m, n, A, lda, tq, U, m, n, ldu, kDriverCwyWidth);
+    if (rc) return rc;
+    return ormbr_run(h, st, 'P', true, m, n, A, lda, tp, VT, n, n, ldvt, kDriverCwyWidth);
+  }
+  DC_CUDA_TRY(cudaEventRecord(h->ev_fork, st));
+  DC_CUDA_TRY(cudaStreamWaitEvent(sd->own_stream, h->ev_fork, 0));
+  rc = ormbr_run(sd, sd->own_stream, 'P', true, m, n, A, lda, tp, VT, n, n, ldvt, kDriverCwyWidth);
+  if (rc) {
+    h->last_error = sd->last_error;
+    return rc;
+  }
   rc = ormbr_run(h, st, 'Q', false, m, n, A, lda, tq, U, m, n, ldu, kDriverCwyWidth);
-  if (rc) return rc;
-  rc = ormbr_run(h, st, 'P', true, m, n, A, lda, tp, VT, n, n, ldvt, kDriverCwyWidth);
+  DC_CUDA_TRY(cudaEventRecord(h->ev_join, sd->own_stream));
+  DC_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_join, 0));
+  merge_err_kernel<<<1, 1, 0, st>>>(h->d_err, sd->d_err);
+  note_launch();
   return rc;
 }
 
@@ -513,6 +555,7 @@ static dcsvd_ctx* make_sub(dcsvd_ctx* h, int sms) {
   s->device = h->device;
   s->sms = sms;
   s->coop_ok = h->coop_ok;
+  s->is_sub = true;
   if (cudaMalloc(&s->d_err, sizeof(int)) != cudaSuccess || cudaMalloc(&s->d_bar, sizeof(unsigned) * kNumBars) != cudaSuccess ||
       cudaMallocHost(&s->h_err, sizeof(int)) != cudaSuccess ||
       cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
@@ -530,6 +573,13 @@ static void free_ctx_resources(dcsvd_ctx* h) {
     delete s;
   }
   h->subs.clear();
+  if (h->side) {
+    free_ctx_resources(h->side);
+    delete h->side;
+    h->side = nullptr;
+    cudaEventDestroy(h->ev_fork);
+    cudaEventDestroy(h->ev_join);
+  }
   for (auto& p : h->pool)
     if (p.ptr) cudaFree(p.ptr);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);

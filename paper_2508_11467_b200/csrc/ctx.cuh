@@ -15,6 +15,9 @@ struct dcsvd_ctx {
   // concurrent sub-contexts for batched SVDs (own stream, pools, status word,
   // barrier counters, SM budget); created lazily by dcsvd_gesdd_batched
   std::vector<dcsvd_ctx*> subs;
+  dcsvd_ctx* side = nullptr;    // second stream + workspace for independent stages (V^T back-transform)
+  bool is_sub = false;          // batch / side sub-context (no further splitting)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // side-stream fork/join
   cudaStream_t own_stream = nullptr;
   int device = 0;
   int sms = 148;
