@@ -265,17 +265,24 @@ struct Geqr2Args {
   long long lda;
   int m, w;
   double* tau;
-  double* part;  // G x 64 partials
+  double* part;    // 2 x G x 64 partials (double-buffered by column parity)
+  double* rowbuf;  // 2 x 64: the pivot row of the current / next column
   unsigned* bar;
   int R1;        // rows per CTA
 };
 
-constexpr int kGeqr2Threads = 256;
+constexpr int kGeqr2Threads = 512;
 
+// One grid barrier per column.  With v = [1; x/den] (LARFG, densecore.py:
+// 114-128) the reflector's w_t = v^T a[:, t] = a[j, t] + (sum_{r>j} x_r a[r, t]) / den,
+// so the norm of x and the cross sums sum_{r>j} x_r a[r, t] are reduced in the
+// same phase, before den is known.  Each CTA keeps its R1-row slab of the
+// panel in shared memory; the owner of row j+1 publishes that row (double
+// buffered, like the partials) for everyone's w.
 __global__ void __launch_bounds__(kGeqr2Threads, 1) geqr2_coop_kernel(Geqr2Args a) {
   extern __shared__ double slab[];  // R1 x w
-  __shared__ double sh_red[32];
   __shared__ double sh_w[64];
+  __shared__ double sh_red[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int g = blockIdx.x, G = gridDim.x;
   const int r0 = g * a.R1, r1 = min(a.m, r0 + a.R1), nr = max(0, r1 - r0);
@@ -286,79 +293,66 @@ __global__ void __launch_bounds__(kGeqr2Threads, 1) geqr2_coop_kernel(Geqr2Args 
     slab[rr + t * R1] = a.A[(r0 + rr) + (long long)t * a.lda];
   }
   __syncthreads();
-  // norm partial of column 0 (rows > 0)
-  {
-    double p = 0.0;
-    for (int rr = tid; rr < nr; rr += blockDim.x)
-      if (r0 + rr > 0) p += slab[rr] * slab[rr];
-    p = block_sum(p, sh_red);
-    if (tid == 0) a.part[g * 64 + 0] = p;
-  }
+  // partials of column c over this CTA's rows r > c into buffer (c & 1):
+  // slot 0 = sum x^2, slot t = sum x * a[r, t] (t > c); row c published.
+  auto partials = [&](int c) {
+    double* part = a.part + (size_t)(c & 1) * G * 64 + (size_t)g * 64;
+    const int lo = max(0, c + 1 - r0);  // first local row > c
+    for (int t = c + warp; t < w; t += nw) {  // warp per slot (t == c: the norm)
+      double s = 0.0;
+      for (int rr = lo + lane; rr < nr; rr += 32) s += slab[rr + c * R1] * slab[rr + t * R1];
+      s = warp_sum(s);
+      if (lane == 0) part[t == c ? 0 : t] = s;
+    }
+    if (c >= r0 && c < r1)
+      for (int t = c + tid; t < w; t += blockDim.x) a.rowbuf[(c & 1) * 64 + t] = slab[(c - r0) + t * R1];
+  };
+  partials(0);
   grid_barrier(a.bar, G, epoch);
   for (int j = 0; j < w; ++j) {
-    // ---- LARFG of column j
-    double p = 0.0;
-    for (int i = tid; i < G; i += blockDim.x) p += a.part[i * 64 + 0];
-    const double nrm2 = block_sum(p, sh_red);
-    // alpha = a[j,j]: the row owner publishes it to global A before the barrier
-    const double alpha = a.A[j + (long long)j * a.lda];
+    const double* part = a.part + (size_t)(j & 1) * G * 64;
+    const double* rowj = a.rowbuf + (j & 1) * 64;
+    // reduce the norm (slot 0) and the cross sums (slots j+1..w-1), warp per slot
+    for (int t = j + warp; t < w; t += nw) {
+      const int slot = t == j ? 0 : t;
+      double s = 0.0;
+      for (int i = lane; i < G; i += 32) s += part[(size_t)i * 64 + slot];
+      s = warp_sum(s);
+      if (lane == 0) sh_w[t] = s;
+    }
+    __syncthreads();
+    const double alpha = rowj[j];
     double tau, beta;
     {
-      const double xn = sqrt(nrm2);
+      const double xn = sqrt(sh_w[j]);
       if (xn == 0.0) { tau = 0.0; beta = alpha; }
       else { beta = -copysign(hypot(alpha, xn), alpha); tau = (beta - alpha) / beta; }
     }
     const double den = alpha - beta;
     if (g == 0 && tid == 0) a.tau[j] = tau;
+    __syncthreads();  // everyone has read sh_w[j]
+    if (tid > j && tid < w) sh_w[tid] = tau != 0.0 ? rowj[tid] + sh_w[tid] / den : 0.0;  // w_t
+    // column j of the slab: beta on row j, essential part x / den below
     for (int rr = tid; rr < nr; rr += blockDim.x) {
       const int r = r0 + rr;
       if (r == j) slab[rr + j * R1] = beta;
       else if (r > j && tau != 0.0) slab[rr + j * R1] /= den;
     }
     __syncthreads();
-    // partial w_t = sum_{r>=j} v_r a[r,t], t in (j, w)
-    if (tau != 0.0 && j + 1 < w) {
+    if (tau != 0.0 && j + 1 < w) {  // a[r, t] -= tau v_r w_t, rows r >= j, columns t > j
+      const int lo = max(0, j - r0);
       for (int t = j + 1 + warp; t < w; t += nw) {
-        double s = 0.0;
-        for (int rr = lane; rr < nr; rr += 32) {
+        const double tw = tau * sh_w[t];
+        for (int rr = lo + lane; rr < nr; rr += 32) {
           const int r = r0 + rr;
-          if (r >= j) s += (r == j ? 1.0 : slab[rr + j * R1]) * slab[rr + t * R1];
-        }
-        s = warp_sum(s);
-        if (lane == 0) a.part[g * 64 + t] = s;
-      }
-    }
-    grid_barrier(a.bar, G, epoch);
-    if (tau != 0.0 && j + 1 < w) {
-      for (int t = j + 1 + warp; t < w; t += nw) {  // warp per column, fixed-order tree
-        double s = 0.0;
-        for (int i = lane; i < G; i += 32) s += a.part[i * 64 + t];
-        s = warp_sum(s);
-        if (lane == 0) sh_w[t] = s;
-      }
-      __syncthreads();
-      for (int idx = tid; idx < nr * (w - j - 1); idx += blockDim.x) {
-        const int rr = idx % nr, t = j + 1 + idx / nr;
-        const int r = r0 + rr;
-        if (r >= j) {
           const double v = r == j ? 1.0 : slab[rr + j * R1];
-          slab[rr + t * R1] -= tau * (v * sh_w[t]);
+          slab[rr + t * R1] -= v * tw;
         }
       }
       __syncthreads();
     }
     if (j + 1 < w) {
-      // publish a[j+1, j+1] (alpha of the next column) and the norm partial
-      double q = 0.0;
-      for (int rr = tid; rr < nr; rr += blockDim.x) {
-        const int r = r0 + rr;
-        const double x = slab[rr + (j + 1) * R1];
-        if (r > j + 1) q += x * x;
-        if (r == j + 1) a.A[r + (long long)(j + 1) * a.lda] = x;
-      }
-      q = block_sum(q, sh_red);
-      // slot 0 was consumed by every CTA before the previous barrier
-      if (tid == 0) a.part[g * 64 + 0] = q;
+      partials(j + 1);
       grid_barrier(a.bar, G, epoch);
     }
   }
@@ -385,7 +379,8 @@ static int geqr2_launch(dcsvd_ctx* h, cudaStream_t st, double* A, long long lda,
   }
   DC_CUDA_TRY(cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned), st));
   Geqr2Args a;
-  a.A = A; a.lda = lda; a.m = m; a.w = w; a.tau = tau; a.part = part; a.bar = h->d_bar; a.R1 = R1;
+  a.A = A; a.lda = lda; a.m = m; a.w = w; a.tau = tau; a.part = part; a.rowbuf = part + (size_t)2 * G * 64;
+  a.bar = h->d_bar; a.R1 = R1;
   void* args[] = {&a};
   DC_CUDA_TRY(cudaLaunchCooperativeKernel((void*)geqr2_coop_kernel, dim3(G), dim3(kGeqr2Threads), args, smem, st));
   note_launch();
@@ -404,12 +399,12 @@ int geqrf_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A
   // columns; the far trailing matrix then takes one W-wide CWY block (DMMA
   // GEMMs with K = W instead of K = nb).
   const int W = std::min(kCwyMaxW, nb * std::max(1, kCwyMaxW / nb));
-  const size_t need = pool_bytes((size_t)m * W, 8) + pool_bytes((size_t)h->sms * 64 + 64, 8) +
+  const size_t need = pool_bytes((size_t)m * W, 8) + pool_bytes((size_t)h->sms * 128 + 128, 8) +
                       pool_bytes(cwy_total_scratch(h->sms, m, n, W), 8);
   int rc = pool_reserve(h, 0, need, st);
   if (rc) return rc;
   double* Y = pool_take<double>(h, 0, (size_t)m * W);
-  double* part = pool_take<double>(h, 0, (size_t)h->sms * 64 + 64);
+  double* part = pool_take<double>(h, 0, (size_t)h->sms * 128 + 128);
   double* scr = pool_take<double>(h, 0, cwy_total_scratch(h->sms, m, n, W));
   for (long long off = 0; off < n; off += W) {
     const int wW = (int)std::min<long long>(W, n - off);
@@ -567,9 +562,9 @@ int block_reflector_run(dcsvd_ctx* h, cudaStream_t st, char side, bool trans, lo
 int geqr2_run(dcsvd_ctx* h, cudaStream_t st, long long m, int w, double* A, long long lda, double* tau) {
   if (m < w) return set_error(h, DCSVD_EINVAL, "panel must be tall, got %lldx%d", m, w);
   if (w < 1 || w > 64) return set_error(h, DCSVD_EINVAL, "GPU panel width must be 1..64, got %d", w);
-  int rc = pool_reserve(h, 0, pool_bytes((size_t)h->sms * 64 + 64, 8), st);
+  int rc = pool_reserve(h, 0, pool_bytes((size_t)h->sms * 128 + 128, 8), st);
   if (rc) return rc;
-  double* part = pool_take<double>(h, 0, (size_t)h->sms * 64 + 64);
+  double* part = pool_take<double>(h, 0, (size_t)h->sms * 128 + 128);
   return geqr2_launch(h, st, A, lda, (int)m, w, tau, part);
 }
 
