@@ -7,7 +7,7 @@ namespace dc {
 
 extern thread_local dcsvd_ctx* t_cur;  // api.cu: handle of the current API call
 
-int g_gemm_route = 0;  // debug: 0 default, 1 no streaming rank-k, 2 also 64x128 C-prefetch tiles
+int g_gemm_route = 0;  // debug: 0 default, 1 no streaming rank-k, 2 also 64x128 C-prefetch tiles, 5 8-byte staging
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -258,7 +258,7 @@ static int launch_cfg(cudaStream_t st, const GemmBatch* b, const GemmDesc* dd, i
       return launch_cfg_v<TA, TB, BM, BN, BK, WM, WN, STAGES, MINB, PFC, false, true>(st, b, dd, nz, max_m, max_n);
     return -1;
   }
-  if (batch_vec_ok(b, dd))
+  if (batch_vec_ok(b, dd) && g_gemm_route != 5)  // route 5 (debug): force 8-byte copies
     return launch_cfg_v<TA, TB, BM, BN, BK, WM, WN, STAGES, MINB, PFC, true, false>(st, b, dd, nz, max_m, max_n);
   return launch_cfg_v<TA, TB, BM, BN, BK, WM, WN, STAGES, MINB, PFC, false, false>(st, b, dd, nz, max_m, max_n);
 }
