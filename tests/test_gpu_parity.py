@@ -808,3 +808,21 @@ def test_c5_shaped_batch(cuda):
     assert (one.sigma - res[3].sigma).abs().max().item() <= 1e-13 * one.sigma[0].item()
     again = g.gesdd_batched(mats)
     assert all(torch.equal(x.sigma, y.sigma) for x, y in zip(res, again))
+
+
+def test_bdsdc_trivial_sizes(cuda):
+    """n = 0 and n = 1 problems return the reference's shapes/values
+    (bdc.py:754-765, 861-880)."""
+    g = _g()
+    r = g.bdsdc(g.BidiagonalProblem(np.zeros(0), np.zeros(0)))
+    assert r.dvals.shape == (0,) and r.w.shape == (0, 0) and r.qfull.shape == (0, 0)
+    r = g.bdsdc(g.BidiagonalProblem(np.array([2.0]), np.zeros(0)))
+    assert_array_equal(r.dvals, [2.0])
+    assert_array_equal(r.w, [[1.0]])
+    assert_array_equal(r.qfull, [[1.0]])
+    assert_array_equal(r.edge_rows, [[1.0], [1.0]])
+    r = g.bdsdc(g.BidiagonalProblem(np.array([-2.0]), np.zeros(0)))
+    assert_array_equal(r.dvals, [2.0])
+    assert_array_equal(r.w, [[-1.0]])
+    with pytest.raises(ValueError):
+        g.gesdd(np.zeros((0, 5)))

@@ -8,7 +8,7 @@ def col(r, c):
     return torch.randn(c, r, dtype=torch.float64, device="cuda").t()
 for (m, n, k) in [(8192, 8192, 8192), (8192, 6000, 6000), (4096, 4096, 2048)]:
     A, B, C = col(m, k), col(k, n), col(m, n)
-    for route in (0, 5):
+    for route in [int(x) for x in (sys.argv[1:] or ['0', '5'])]:
         lib.dcsvd_debug_gemm_route(route)
         f = lambda: lib.dcsvd_dgemm(h, 0, 0, m, n, k, 1.0, _lib.ptr(A), m, _lib.ptr(B), k, 0.0, _lib.ptr(C), m, st)
         f(); torch.cuda.synchronize()
