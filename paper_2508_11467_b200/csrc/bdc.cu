@@ -1142,6 +1142,7 @@ int bdsdc_run(dcsvd_ctx* h, cudaStream_t st, long long n_, const double* d, cons
   const int n = (int)n_;
   const int ncols = n + (bordered ? 1 : 0);
   if (n < 0) return set_error(h, DCSVD_EINVAL, "n must be >= 0");
+  if (ncols == 0) return 0;  // 0 x 0 problem: empty outputs (bdc.py:754-765)
   std::vector<TreeNode> nodes;
   int H = 0;
   if (n > 0) H = build_tree(nodes, 0, n, bordered ? 1 : 0, leaf);

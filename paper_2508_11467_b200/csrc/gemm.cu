@@ -274,10 +274,6 @@ static int launch_sized(cudaStream_t st, const GemmBatch* b, const GemmDesc* dd,
   const long long tiles64x128 = (long long)((max_m + 63) / 64) * ((max_n + 127) / 128) * nz;
   if (g_gemm_route == 2 && beta_nz)  // debug routing experiments (dcsvd_debug_gemm_route)
     return launch_cfg<TA, TB, 64, 128, 16, 2, 2, 3, 2, true>(st, b, dd, nz, max_m, max_n);
-  if (g_gemm_route == 6 && tiles64x128 >= 2 * 148 && max_k >= 128)
-    return launch_cfg<TA, TB, 64, 128, 32, 2, 2, 2, 2, false>(st, b, dd, nz, max_m, max_n);
-  if (g_gemm_route == 7 && tiles64x128 >= 2 * 148 && max_k >= 128)
-    return launch_cfg<TA, TB, 64, 128, 16, 2, 2, 4, 2, false>(st, b, dd, nz, max_m, max_n);
   if (tiles64x128 >= 2 * 148 && max_k >= 128)
     return launch_cfg<TA, TB, 64, 128, 16, 2, 2, 3, 2, false>(st, b, dd, nz, max_m, max_n);
   if (beta_nz && max_k <= 64)  // rank-k updates: C read-modify-write dominates -> prefetch C
