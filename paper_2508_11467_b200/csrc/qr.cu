@@ -67,9 +67,24 @@ constexpr int kTinvSolveWarps = 16;
 
 __global__ void __launch_bounds__(32 * kTinvSolveWarps) cwy_tinv_solve_kernel(const double* __restrict__ Tinv, int w,
                                                                               int trans, double* __restrict__ Top) {
-  extern __shared__ double ts[];  // w x w (ld w)
-  for (int i = threadIdx.x; i < w * w; i += blockDim.x) ts[i] = Tinv[i];
-  __syncthreads();
+  extern __shared__ double ts[];  // w x w (ld w); diagonal replaced by its reciprocal
+  {
+    const int tot = w * w;
+    if ((reinterpret_cast<uintptr_t>(Tinv) & 15) == 0) {  // 16-byte staging, 4 loads in flight
+      const double2* src = reinterpret_cast<const double2*>(Tinv);
+      double2* dst = reinterpret_cast<double2*>(ts);
+      const int n2 = tot >> 1;
+#pragma unroll 4
+      for (int i = threadIdx.x; i < n2; i += blockDim.x) dst[i] = src[i];
+      if ((tot & 1) && threadIdx.x == 0) ts[tot - 1] = Tinv[tot - 1];
+    } else {
+#pragma unroll 4
+      for (int i = threadIdx.x; i < tot; i += blockDim.x) ts[i] = Tinv[i];
+    }
+    __syncthreads();
+    if (threadIdx.x < w) ts[threadIdx.x * (w + 1)] = 1.0 / ts[threadIdx.x * (w + 1)];  // no division in the chain
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x * kTinvSolveWarps + (threadIdx.x >> 5);
   if (c >= w) return;
@@ -83,7 +98,7 @@ __global__ void __launch_bounds__(32 * kTinvSolveWarps) cwy_tinv_solve_kernel(co
 #pragma unroll
     for (int q = 0; q < kCwyMaxW / 32; ++q)
       if (q == qi) ti = t[q];
-    ti = __shfl_sync(0xffffffffu, ti, li) / col[i];
+    ti = __shfl_sync(0xffffffffu, ti, li) * col[i];
 #pragma unroll
     for (int q = 0; q < kCwyMaxW / 32; ++q) {
       const int l = lane + 32 * q;
