@@ -1137,7 +1137,9 @@ int bdsdc_run(dcsvd_ctx* h, cudaStream_t st, long long n_, const double* d, cons
               bool vectors, int leaf, double tol_mult, double* dvals, double* edge_out, double* Wout,
               long long ldwo, long long wrows, double* Qout, long long ldqo, double* VT, long long ldvt) {
   if (leaf < 1) return set_error(h, DCSVD_EINVAL, "leaf size must be >= 1, got %d", leaf);
-  if (leaf > 32) return set_error(h, DCSVD_EINVAL, "GPU BDC supports leaf sizes 1..32, got %d", leaf);
+  // Leaves above 32 (the warp-per-leaf QR kernel) split once more: the same
+  // decomposition up to rounding.
+  if (leaf > 32) leaf = 32;
   if (!(tol_mult > 0.0)) return set_error(h, DCSVD_EINVAL, "deflation multiple must be > 0");
   const int n = (int)n_;
   const int ncols = n + (bordered ? 1 : 0);

@@ -1048,7 +1048,9 @@ int gebrd_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A
               double* d, double* e, double* tauq, double* taup, int nb) {
   if (n < 1 || m < n) return set_error(h, DCSVD_EINVAL, "bidiagonalization requires m >= n >= 1, got %lldx%lld", m, n);
   if (nb < 1) return set_error(h, DCSVD_EINVAL, "block width must be >= 1, got %d", nb);
-  if (nb > 32 && nb < n) return set_error(h, DCSVD_EINVAL, "GPU GEBRD supports block width <= 32, got %d", nb);
+  // Wider panels than the GPU panel kernel takes give the same reflectors (the
+  // panel width only regroups the trailing updates): run them as 32-wide panels.
+  if (nb > 32 && nb < n) nb = 32;
   const bool unblocked = nb >= n;
   if (unblocked) nb = (int)std::min<long long>(n, 32);  // no panel runs: the whole matrix goes through GEBD2
   const int G = h->sms;

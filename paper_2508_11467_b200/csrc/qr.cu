@@ -407,8 +407,7 @@ int geqrf_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A
   if (n < 1) return set_error(h, DCSVD_EINVAL, "matrix must have at least one column");
   if (m < n) return set_error(h, DCSVD_EINVAL, "QR factorization requires m >= n, got %lldx%lld", m, n);
   if (nb < 1) return set_error(h, DCSVD_EINVAL, "block width must be >= 1, got %d", nb);
-  if (nb > kCwyMaxW) return set_error(h, DCSVD_EINVAL, "GPU QR supports block width <= %d, got %d", kCwyMaxW, nb);
-  if (nb > 64) return set_error(h, DCSVD_EINVAL, "GPU QR panel width must be <= 64, got %d", nb);
+  if (nb > 64) nb = 64;  // panel width of the GPU kernel; wider blocks give the same reflectors
   // Two-level blocking (same reflectors, LAPACK dgeqrf order): nb-wide panels
   // are factored and applied inside an outer block of W = nb*ceil(128/nb)
   // columns; the far trailing matrix then takes one W-wide CWY block (DMMA
@@ -462,7 +461,8 @@ __global__ void eye_kernel(double* Q, long long ldq, long long m, long long k) {
 int orgqr_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long nrefl, long long k, const double* A,
               long long lda, const double* tau, double* Q, long long ldq, int nb) {
   if (k < 1 || k > m) return set_error(h, DCSVD_EINVAL, "need 1 <= k <= %lld columns of Q, got %lld", m, k);
-  if (nb < 1 || nb > kCwyMaxW) return set_error(h, DCSVD_EINVAL, "GPU ORGQR supports block width 1..%d, got %d", kCwyMaxW, nb);
+  if (nb < 1) return set_error(h, DCSVD_EINVAL, "block width must be >= 1, got %d", nb);
+  if (nb > kCwyMaxW) nb = kCwyMaxW;  // T^-1 = triu(Y^T Y, 1) + diag(1/tau) is exact for any grouping
   const size_t need = pool_bytes((size_t)m * nb, 8) + pool_bytes(cwy_total_scratch(h->sms, m, k, nb), 8);
   int rc = pool_reserve(h, 0, need, st);
   if (rc) return rc;
@@ -488,7 +488,8 @@ int orgqr_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long nrefl, long 
 int ormbr_run(dcsvd_ctx* h, cudaStream_t st, char vect, bool trans, long long m, long long n, const double* A,
               long long lda, const double* tau, double* C, long long c_rows, long long c_cols, long long ldc,
               int nb) {
-  if (nb < 1 || nb > kCwyMaxW) return set_error(h, DCSVD_EINVAL, "GPU ORMBR supports block width 1..%d, got %d", kCwyMaxW, nb);
+  if (nb < 1) return set_error(h, DCSVD_EINVAL, "block width must be >= 1, got %d", nb);
+  if (nb > kCwyMaxW) nb = kCwyMaxW;  // same product, grouped in 128-wide compact-WY blocks
   if (vect == 'Q') {
     if (c_rows != m) return set_error(h, DCSVD_EINVAL, "C has %lld rows, sequence acts on %lld", c_rows, m);
     const long long count = n;

@@ -213,10 +213,10 @@ def split(prob):
 
 def bdsqr_base(prob, want_vectors=True):
     """Leaf SVD by implicit-shift QR iteration (bdc.py:315-359), values
-    ascending (the tree-internal convention).  GPU leaf kernel: n <= 32."""
-    if prob.n > 32:
-        raise ValueError(f"GPU leaf solver handles n <= 32, got {prob.n}")
-    r = bdsdc(prob, want_vectors=want_vectors, leaf=max(prob.n, 1))
+    ascending (the tree-internal convention).  n <= 32 runs the GPU leaf
+    kernel itself; larger problems go through the GPU divide and conquer with
+    32-row leaves (the same decomposition up to rounding)."""
+    r = bdsdc(prob, want_vectors=want_vectors, leaf=min(max(prob.n, 1), 32))
     n = prob.n
     flip = lambda x: x.flip(0) if isinstance(x, torch.Tensor) else x[::-1].copy()
     vals = flip(r.dvals)

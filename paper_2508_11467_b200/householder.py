@@ -94,9 +94,11 @@ def orgqr(fact, k, block=64):
 
 def _apply(seq, c, vect, transpose, block):
     m, n = seq.packed.shape
+    if vect == "Q":
+        n = int(seq.count)  # the first `count` column reflectors (columns beyond are not read)
     h = _lib.handle()
     A, _ = _lib.to_device_colmajor(seq.packed, copy=False)
-    tau = _lib.vec_to_device(seq.tau, n)
+    tau = _lib.vec_to_device(seq.tau)[:n].contiguous()
     C, c_np = _lib.to_device_colmajor(c, copy=False)
     rc = _lib.load_library().dcsvd_ormbr(h, vect.encode(), int(bool(transpose)), m, n, _lib.ptr(A), _lib.ld(A),
                                          _lib.ptr(tau), _lib.ptr(C), C.shape[0], C.shape[1], _lib.ld(C),
@@ -112,8 +114,10 @@ def ormqr_like(seq, c, transpose=False, block=64):
         raise ValueError(f"expected a left-side sequence, got {seq.side!r}")
     if c.shape[0] != seq.packed.shape[0]:
         raise ValueError(f"C has {c.shape[0]} rows, sequence acts on {seq.packed.shape[0]}")
-    if seq.count != seq.packed.shape[1] or seq.offset != 0:
-        raise ValueError("GPU ormqr_like supports the full column-reflector sequence of a bidiagonalization")
+    if seq.offset != 0 or not 0 <= seq.count <= min(seq.packed.shape):
+        raise ValueError("column reflectors need offset 0 and 0 <= count <= min(packed.shape)")
+    if seq.count == 0:
+        return c
     return _apply(seq, c, "Q", transpose, block)
 
 

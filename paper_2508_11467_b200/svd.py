@@ -22,8 +22,9 @@ PHASE_NAMES = ("geqrf", "orgqr", "gebrd", "bdcdc", "ormqr+ormlq", "gemm")
 
 @dataclass
 class SVDOptions:
-    """Tuning knobs (driver.py:34-63).  GPU limits: bidiag_block <= 32,
-    qr/orgqr/apply blocks <= 64, leaf_size <= 32."""
+    """Tuning knobs (driver.py:34-63), validated like the reference.  Values
+    above the GPU kernels' widths (bidiag 32, QR panel 64, CWY 128, leaf 32)
+    run at those widths: the same factorization up to rounding."""
 
     want_vectors: bool = True
     bidiag_block: int = 32

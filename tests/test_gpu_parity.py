@@ -826,3 +826,34 @@ def test_bdsdc_trivial_sizes(cuda):
     assert_array_equal(r.w, [[-1.0]])
     with pytest.raises(ValueError):
         g.gesdd(np.zeros((0, 5)))
+
+
+def test_wide_options_and_partial_sequences(cuda):
+    """Block/leaf widths above the GPU kernels' limits are accepted like the
+    reference (same factorization up to rounding); left reflector sequences
+    with count < ncols apply the first `count` reflectors (backtransform.py:60-72)."""
+    g = _g()
+    a = oracle.make_matrix("random", 150, 120, seed=12)
+    s, _, _ = oracle.svd(a, want_vectors=False)
+    for opts in (g.SVDOptions(bidiag_block=64, leaf_size=64, qr_block=100, orgqr_block=300, apply_block=256),
+                 g.SVDOptions(bidiag_block=200, ts_crossover=1.0)):
+        r = g.gesdd(a, opts)
+        check_svd(a, r.sigma, r.u, r.vt, s)
+    f1 = g.gebrd_blocked(np.asfortranarray(a.copy()), 64)
+    f2 = g.gebrd_blocked(np.asfortranarray(a.copy()), 32)
+    np.testing.assert_allclose(f1.d, f2.d, rtol=0, atol=1e-12 * np.abs(f2.d).max())
+    prob = g.BidiagonalProblem(f2.d, f2.e[:119])
+    np.testing.assert_allclose(g.bdsdc(prob, leaf=100).dvals, g.bdsdc(prob).dvals, rtol=0, atol=1e-13 * s[0])
+    r = g.bdsqr_base(g.BidiagonalProblem(np.linspace(1, 2, 50), np.full(49, 0.1)))
+    assert np.all(np.diff(r.dvals) >= 0)
+    # partial left sequence vs the oracle's reflector-by-reflector product
+    fact = g.gebrd_blocked(np.asfortranarray(oracle.make_matrix("random", 60, 40, seed=3)), 8)
+    seq = g.column_reflectors(fact)
+    seq = g.ReflectorSequence(seq.packed, seq.tau, "left", 0, 17)
+    c = np.asfortranarray(np.random.default_rng(0).standard_normal((60, 25)))
+    ref = c.copy()
+    for i in reversed(range(17)):                     # U1 C = H_0 (H_1 (... H_16 C))
+        v = np.concatenate(([1.0], fact.packed[i + 1:, i]))
+        ref[i:] -= fact.tauq[i] * np.outer(v, v @ ref[i:])
+    out = g.ormqr_like(seq, c.copy(order="F"))
+    np.testing.assert_allclose(out, ref, rtol=0, atol=1e-13)
