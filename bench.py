@@ -207,6 +207,7 @@ def run_c4(args, dcs, _lib, torch, dist, ws, rank, local):
     torch.cuda.synchronize()
     s, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = _lib.launch_count()
+    _lib.set_stats(True)
     with ClockSampler(local) as clk:
         s.record()
         for _ in range(args.steps):
@@ -214,6 +215,11 @@ def run_c4(args, dcs, _lib, torch, dist, ws, rank, local):
         e1.record()
         torch.cuda.synchronize()
     t_ms = s.elapsed_time(e1) / args.steps
+    g_ms, g_flops, g_n = _lib.get_stats(2)
+    _lib.set_stats(False)
+    peaks, _ = load_peaks()
+    dmma_peak = 148 * 128 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+    g_ach = g_flops / (g_ms * 1e-3) / 1e12 if g_ms > 0 else None
     vals = r.dvals.cpu().numpy()
     w = r.w
     gram = _lib.colmajor_empty(n, n)
@@ -236,6 +242,18 @@ def run_c4(args, dcs, _lib, torch, dist, ws, rank, local):
                      "values_only_bitwise_equal": bool(np.array_equal(rv.dvals.cpu().numpy(), vals))},
         "values_only_seconds": t_vo,
         "gpu_launches": int((_lib.launch_count() - l0) // max(args.steps, 1)),
+        "roofline": {
+            "kernel": "dgemm_kernel, grouped BDC merge products (gathered columns, device descriptors)",
+            "bound": "tensor", "achieved": g_ach, "peak": dmma_peak, "unit": "TFLOP/s",
+            "frac": (g_ach / dmma_peak) if g_ach else None,
+            "peak_source": "FP64 DMMA peak 148 SMs x 128 flop/clk at sm_max_mhz (MEASURED_PEAKS.json)",
+            "traffic": None,
+            "algorithmic_flops_per_step": g_flops / max(args.steps, 1),
+            "launches_per_step": g_n / max(args.steps, 1),
+            "share_of_step": (g_ms / args.steps) / t_ms if t_ms > 0 else None,
+            "note": "flops = sum 2 m n k of the structured merge products, counted on the device from the "
+                    "post-deflation sizes; heavy deflation makes the merges small and latency-bound",
+        },
         "clocks": clk.summary(),
         "cpu_baseline": {"value": float(F / float(z["ref_seconds_values_only"]) / 1e9), "unit": "GFLOP/s", "cores": 7,
                          "kind": "reference", "seconds": float(z["ref_seconds_values_only"]),
@@ -312,10 +330,11 @@ def main():
     t_ms = ev0.elapsed_time(ev1) / args.steps
     lab_ms, lab_bytes, lab_n = _lib.get_stats(0)
     gem_ms, gem_flops, gem_n = _lib.get_stats(1)
+    bdc_ms, bdc_flops, bdc_n = _lib.get_stats(2)  # BDC merge GEMMs (device-counted flops)
+    gem_ms, gem_flops, gem_n = gem_ms + bdc_ms, gem_flops + bdc_flops, gem_n + bdc_n
     lib = _lib.load_library()
     lib.dcsvd_debug_batch_streams.restype = ctypes.c_int
-    streams = max(1, lib.dcsvd_debug_batch_streams(_lib.handle()))  # concurrent launches overlap
-    lab_ms, gem_ms = lab_ms / streams, gem_ms / streams
+    streams = max(1, lib.dcsvd_debug_batch_streams(_lib.handle()))
     _lib.set_stats(False)
     if ws > 1:
         tt = torch.tensor([t_ms], device=f"cuda:{local}")
@@ -377,8 +396,8 @@ def main():
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     achieved = (lab_bytes / (lab_ms * 1e-3) / 1e9) if lab_ms > 0 else None
     ncu = load_ncu_traffic() or {}
-    note_streams = f" (batched: {streams} concurrent streams; per-family busy time = sum of launch durations / {streams})" \
-        if streams > 1 else ""
+    note_streams = (f"; batched: {streams} concurrent streams" if streams > 1 else "") + \
+        "; family time = wall-clock union of its launch intervals across streams"
     roof_lab = {
         "kernel": "labrd4_kernel + labrd2_kernel (GEBRD panels: 2 GEMVs per column over the trailing matrix)",
         "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -390,14 +409,14 @@ def main():
         "algorithmic_bytes_per_step": lab_bytes / max(args.steps, 1),
         "launches_per_step": lab_n / max(args.steps, 1),
         "share_of_step": (lab_ms / args.steps) / t_ms if t_ms > 0 else None,
-        "note": "achieved = algorithmic GEMV bytes (8 sum_k [(m'-k)(n'-k-1) + (m'-k-1)(n'-k-1)] per panel) / CUDA-event "
-                "durations of the panel launches on their stream" + note_streams,
+        "note": "achieved = algorithmic GEMV bytes (8 sum_k [(m'-k)(n'-k-1) + (m'-k-1)(n'-k-1)] per panel) / time of "
+                "the panel launches (CUDA events on their streams)" + note_streams,
     }
     dmma_peak = 148 * 128 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
     gem_achieved = (gem_flops / (gem_ms * 1e-3) / 1e12) if gem_ms > 0 else None
     roof_gem = {
-        "kernel": "dgemm_kernel + rankk_stream_kernel (DMMA GEMMs with host descriptors: GEBRD trailing, CWY "
-                  "ORMBR/GEQRF/ORGQR, TS recombination; BDC merge products not counted)",
+        "kernel": "dgemm_kernel + rankk_stream_kernel (all DMMA GEMMs: GEBRD trailing, CWY ORMBR/GEQRF/ORGQR, "
+                  "TS recombination, BDC merge products)",
         "bound": "tensor", "achieved": gem_achieved, "peak": dmma_peak, "unit": "TFLOP/s",
         "frac": (gem_achieved / dmma_peak) if gem_achieved else None,
         "peak_source": "FP64 DMMA peak 148 SMs x 128 flop/clk at sm_max_mhz (MEASURED_PEAKS.json); cuBLAS DGEMM "
@@ -406,7 +425,7 @@ def main():
         "algorithmic_flops_per_step": gem_flops / max(args.steps, 1),
         "launches_per_step": gem_n / max(args.steps, 1),
         "share_of_step": (gem_ms / args.steps) / t_ms if t_ms > 0 else None,
-        "note": "achieved = 2mnk per launch / CUDA-event durations" + note_streams,
+        "note": "achieved = sum 2mnk / time of the GEMM launches (CUDA events on their streams)" + note_streams,
     }
     roof, roof2 = (roof_lab, roof_gem) if lab_ms >= gem_ms else (roof_gem, roof_lab)
     line = {

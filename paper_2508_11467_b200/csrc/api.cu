@@ -372,7 +372,7 @@ int dcsvd_create(dcsvd_handle* out, int device) {
   h->sms = prop.multiProcessorCount;
   h->coop_ok = prop.cooperativeLaunch;
   if (cudaMalloc(&h->d_err, sizeof(int)) != cudaSuccess || cudaMalloc(&h->d_bar, sizeof(unsigned) * kNumBars) != cudaSuccess ||
-      cudaMallocHost(&h->h_err, sizeof(int)) != cudaSuccess) {
+      cudaMallocHost(&h->h_err, sizeof(int)) != cudaSuccess || cudaMalloc(&h->d_flops, sizeof(double)) != cudaSuccess) {
     delete h;
     return DCSVD_ECUDA;
   }
@@ -404,7 +404,12 @@ int dcsvd_set_stats(dcsvd_handle h, int enable) {
   }
   h->stats.clear();
   h->stats_on = enable != 0;
+  if (h->d_flops) cudaMemset(h->d_flops, 0, sizeof(double));
+  if (!h->ev_stats0) cudaEventCreate(&h->ev_stats0);
+  cudaEventRecord(h->ev_stats0, 0);  // after the device synchronize above: precedes every record
+  cudaEventSynchronize(h->ev_stats0);
   for (auto* sub : h->subs) dcsvd_set_stats(sub, enable);  // batched sub-contexts record too
+  if (h->side) dcsvd_set_stats(h->side, enable);
   return 0;
 }
 
@@ -427,27 +432,49 @@ int dcsvd_debug_stat_records(dcsvd_handle h, int kind, double* ms, double* work,
   return c;
 }
 
+// Kernel-family timing: `ms` = wall-clock time during which at least one
+// launch of the family was running (union of the launch intervals over this
+// handle's streams, its side stream and batch sub-contexts), `work` = summed
+// algorithmic work, `launches` = count.
+static void collect_stats(dcsvd_ctx* h, cudaEvent_t origin, int kind, std::vector<std::pair<double, double>>& iv,
+                          double& work, long long& count) {
+  for (auto& r : h->stats) {
+    if (r.kind != kind) continue;
+    float a = 0.f, b = 0.f;
+    if (cudaEventElapsedTime(&a, origin, r.a) == cudaSuccess && cudaEventElapsedTime(&b, origin, r.b) == cudaSuccess)
+      iv.emplace_back(a, b);
+    work += r.work;
+    ++count;
+  }
+  if (kind == 2 && h->d_flops) {  // device-counted flops of the BDC merge GEMMs
+    double f = 0.0;
+    cudaMemcpy(&f, h->d_flops, sizeof(double), cudaMemcpyDeviceToHost);
+    work += f;
+  }
+  for (auto* sub : h->subs) collect_stats(sub, origin, kind, iv, work, count);
+  if (h->side) collect_stats(h->side, origin, kind, iv, work, count);
+}
+
 int dcsvd_get_stats(dcsvd_handle h, int kind, double* ms, double* work, long long* launches) {
   if (!h) return DCSVD_EINVAL;
   cudaSetDevice(h->device);
   cudaDeviceSynchronize();
-  double t = 0.0, w = 0.0;
+  std::vector<std::pair<double, double>> iv;
+  double w = 0.0;
   long long c = 0;
-  for (auto& r : h->stats) {
-    if (r.kind != kind) continue;
-    float x = 0.f;
-    if (cudaEventElapsedTime(&x, r.a, r.b) == cudaSuccess) t += x;
-    w += r.work;
-    ++c;
+  if (h->ev_stats0) collect_stats(h, h->ev_stats0, kind, iv, w, c);
+  std::sort(iv.begin(), iv.end());
+  double t = 0.0, cur_a = 0.0, cur_b = -1.0;
+  for (auto& p : iv) {
+    if (p.first > cur_b) {
+      if (cur_b > cur_a) t += cur_b - cur_a;
+      cur_a = p.first;
+      cur_b = p.second;
+    } else if (p.second > cur_b) {
+      cur_b = p.second;
+    }
   }
-  for (auto* sub : h->subs) {  // batched sub-contexts (concurrent streams: times add up per stream)
-    double st = 0.0, sw = 0.0;
-    long long sc = 0;
-    dcsvd_get_stats(sub, kind, &st, &sw, &sc);
-    t += st;
-    w += sw;
-    c += sc;
-  }
+  if (cur_b > cur_a) t += cur_b - cur_a;
   if (ms) *ms = t;
   if (work) *work = w;
   if (launches) *launches = c;
@@ -557,6 +584,7 @@ static dcsvd_ctx* make_sub(dcsvd_ctx* h, int sms) {
   s->coop_ok = h->coop_ok;
   s->is_sub = true;
   if (cudaMalloc(&s->d_err, sizeof(int)) != cudaSuccess || cudaMalloc(&s->d_bar, sizeof(unsigned) * kNumBars) != cudaSuccess ||
+      cudaMalloc(&s->d_flops, sizeof(double)) != cudaSuccess ||
       cudaMallocHost(&s->h_err, sizeof(int)) != cudaSuccess ||
       cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete s;
@@ -564,6 +592,7 @@ static dcsvd_ctx* make_sub(dcsvd_ctx* h, int sms) {
   }
   cudaMemset(s->d_err, 0, sizeof(int));
   cudaMemset(s->d_bar, 0, sizeof(unsigned) * kNumBars);
+  cudaMemset(s->d_flops, 0, sizeof(double));
   return s;
 }
 
@@ -586,6 +615,7 @@ static void free_ctx_resources(dcsvd_ctx* h) {
   cudaFree(h->d_err);
   cudaFree(h->d_bar);
   cudaFreeHost(h->h_err);
+  if (h->d_flops) cudaFree(h->d_flops);
 }
 
 // Independent SVDs run concurrently: `conc` host threads each drive one

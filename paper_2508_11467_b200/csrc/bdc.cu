@@ -971,7 +971,7 @@ __global__ void __launch_bounds__(kOrderThreads) bdc_order_kernel(const MergeDes
 __global__ void bdc_gemm_desc_kernel(const MergeDesc* __restrict__ merges, const MergeMeta* __restrict__ meta,
                                      int nmerges, BdcBufs B, const double* W, const double* Q, long long ld,
                                      const double* Us, const double* Vs, double* S3, double* S4,
-                                     GemmDesc* __restrict__ out) {
+                                     GemmDesc* __restrict__ out, double* flops) {
   const int mi = blockIdx.x * blockDim.x + threadIdx.x;
   if (mi >= nmerges) return;
   const MergeDesc M = merges[mi];
@@ -1006,6 +1006,11 @@ __global__ void bdc_gemm_desc_kernel(const MergeDesc* __restrict__ merges, const
   g.B = Vs + (r0 + mt.nFq) + (long long)r0 * ld;
   g.C = S4 + r0 + nl + 1;
   out[4 * mi + 3] = g;
+  if (flops) {  // stats: 2 m n k of the four products (integers: exact in fp64)
+    double f = 0.0;
+    for (int q = 0; q < 4; ++q) f += 2.0 * out[4 * mi + q].m * (double)out[4 * mi + q].n * out[4 * mi + q].k;
+    atomicAdd(flops, f);
+  }
 }
 
 // Deflated columns, unit row, null column into scratch.  One warp per output
@@ -1267,9 +1272,12 @@ int bdsdc_run(dcsvd_ctx* h, cudaStream_t st, long long n_, const double* d, cons
     DC_CUDA_TRY(cudaGetLastError());
     if (vectors) {
       GemmDesc* gd = d_gd + 4 * level_off[lv];
-      bdc_gemm_desc_kernel<<<(nm + 127) / 128, 128, 0, st>>>(md, mm, nm, B, W, Q, ld, Us, Vs, S3, S4, gd);
+      bdc_gemm_desc_kernel<<<(nm + 127) / 128, 128, 0, st>>>(md, mm, nm, B, W, Q, ld, Us, Vs, S3, S4, gd,
+                                                            h->stats_on ? h->d_flops : nullptr);
       note_launch();
+      const int sidx = stat_begin(h, 2, 0.0, st);  // flops arrive through h->d_flops
       rc = gemm_launch_device(st, false, false, gd, 4 * nm, maxn, maxn);
+      stat_end(h, sidx, st);
       if (rc) return rc;
       bdc_defl_copy_kernel<<<dim3((maxn + 1 + 7) / 8, nm), 256, 0, st>>>(md, mm, B, W, Q, ld, S3, S4);
       note_launch();

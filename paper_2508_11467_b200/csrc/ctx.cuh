@@ -26,6 +26,7 @@ struct dcsvd_ctx {
   int* d_err = nullptr;         // device status word (dc::DevErr)
   unsigned* d_bar = nullptr;    // grid-barrier counters (kNumBars)
   int* h_err = nullptr;         // pinned mirror of d_err
+  double* d_flops = nullptr;    // device-side flop counter of the BDC merge GEMMs (stats kind 2)
   DevPool pool[3];              // 0: stage scratch, 1: driver buffers, 2: bdc
   // optional per-kernel-family timing (bench roofline): CUDA events around
   // each launch of a family, with its algorithmic bytes/flops
@@ -37,6 +38,7 @@ struct dcsvd_ctx {
   };
   std::vector<StatRec> stats;
   std::vector<cudaEvent_t> ev_free;  // recycled timing events (no create/destroy per launch)
+  cudaEvent_t ev_stats0 = nullptr;    // recorded when stats are (re)enabled: time origin of the records
 };
 
 namespace dc {
