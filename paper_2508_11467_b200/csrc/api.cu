@@ -372,7 +372,7 @@ int dcsvd_create(dcsvd_handle* out, int device) {
   h->sms = prop.multiProcessorCount;
   h->coop_ok = prop.cooperativeLaunch;
   if (cudaMalloc(&h->d_err, sizeof(int)) != cudaSuccess || cudaMalloc(&h->d_bar, sizeof(unsigned) * kNumBars) != cudaSuccess ||
-      cudaMallocHost(&h->h_err, sizeof(int)) != cudaSuccess || cudaMalloc(&h->d_flops, sizeof(double)) != cudaSuccess) {
+      cudaMallocHost(&h->h_err, sizeof(int)) != cudaSuccess || cudaMalloc(&h->d_flops, 2 * sizeof(double)) != cudaSuccess) {
     delete h;
     return DCSVD_ECUDA;
   }
@@ -404,7 +404,7 @@ int dcsvd_set_stats(dcsvd_handle h, int enable) {
   }
   h->stats.clear();
   h->stats_on = enable != 0;
-  if (h->d_flops) cudaMemset(h->d_flops, 0, sizeof(double));
+  if (h->d_flops) cudaMemset(h->d_flops, 0, 2 * sizeof(double));
   if (!h->ev_stats0) cudaEventCreate(&h->ev_stats0);
   cudaEventRecord(h->ev_stats0, 0);  // after the device synchronize above: precedes every record
   cudaEventSynchronize(h->ev_stats0);
@@ -446,9 +446,9 @@ static void collect_stats(dcsvd_ctx* h, cudaEvent_t origin, int kind, std::vecto
     work += r.work;
     ++count;
   }
-  if (kind == 2 && h->d_flops) {  // device-counted flops of the BDC merge GEMMs
+  if ((kind == 2 || kind == 3) && h->d_flops) {  // device-counted BDC merge flops / deflated-column bytes
     double f = 0.0;
-    cudaMemcpy(&f, h->d_flops, sizeof(double), cudaMemcpyDeviceToHost);
+    cudaMemcpy(&f, h->d_flops + (kind - 2), sizeof(double), cudaMemcpyDeviceToHost);
     work += f;
   }
   for (auto* sub : h->subs) collect_stats(sub, origin, kind, iv, work, count);
@@ -584,7 +584,7 @@ static dcsvd_ctx* make_sub(dcsvd_ctx* h, int sms) {
   s->coop_ok = h->coop_ok;
   s->is_sub = true;
   if (cudaMalloc(&s->d_err, sizeof(int)) != cudaSuccess || cudaMalloc(&s->d_bar, sizeof(unsigned) * kNumBars) != cudaSuccess ||
-      cudaMalloc(&s->d_flops, sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&s->d_flops, 2 * sizeof(double)) != cudaSuccess ||
       cudaMallocHost(&s->h_err, sizeof(int)) != cudaSuccess ||
       cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete s;
@@ -592,7 +592,7 @@ static dcsvd_ctx* make_sub(dcsvd_ctx* h, int sms) {
   }
   cudaMemset(s->d_err, 0, sizeof(int));
   cudaMemset(s->d_bar, 0, sizeof(unsigned) * kNumBars);
-  cudaMemset(s->d_flops, 0, sizeof(double));
+  cudaMemset(s->d_flops, 0, 2 * sizeof(double));
   return s;
 }
 

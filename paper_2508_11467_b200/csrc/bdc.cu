@@ -1010,6 +1010,7 @@ __global__ void bdc_gemm_desc_kernel(const MergeDesc* __restrict__ merges, const
     double f = 0.0;
     for (int q = 0; q < 4; ++q) f += 2.0 * out[4 * mi + q].m * (double)out[4 * mi + q].n * out[4 * mi + q].k;
     atomicAdd(flops, f);
+    atomicAdd(flops + 1, 16.0 * mt.nd * (double)(M.n + ncols));  // deflated W/Q columns read + written
   }
 }
 
@@ -1279,10 +1280,16 @@ int bdsdc_run(dcsvd_ctx* h, cudaStream_t st, long long n_, const double* d, cons
       rc = gemm_launch_device(st, false, false, gd, 4 * nm, maxn, maxn);
       stat_end(h, sidx, st);
       if (rc) return rc;
+      const int sc = stat_begin(h, 3, 0.0, st);  // bytes arrive through h->d_flops[1]
       bdc_defl_copy_kernel<<<dim3((maxn + 1 + 7) / 8, nm), 256, 0, st>>>(md, mm, B, W, Q, ld, S3, S4);
+      stat_end(h, sc, st);
       note_launch();
       if (lv < H) {
+        double cb = 0.0;
+        for (const auto& mg : levels[lv]) cb += 16.0 * ((double)mg.n * mg.n + (double)(mg.n + mg.bordered) * (mg.n + mg.bordered));
+        const int sb = stat_begin(h, 3, cb, st);
         bdc_copyback_kernel<<<dim3((maxn + 7) / 8, nm), 256, 0, st>>>(md, S3, S4, ld, W, Q);
+        stat_end(h, sb, st);
         note_launch();
       }
       DC_CUDA_TRY(cudaGetLastError());

@@ -26,7 +26,7 @@ struct dcsvd_ctx {
   int* d_err = nullptr;         // device status word (dc::DevErr)
   unsigned* d_bar = nullptr;    // grid-barrier counters (kNumBars)
   int* h_err = nullptr;         // pinned mirror of d_err
-  double* d_flops = nullptr;    // device-side flop counter of the BDC merge GEMMs (stats kind 2)
+  double* d_flops = nullptr;    // device-side counters: [0] BDC merge GEMM flops (stats kind 2), [1] deflated-column bytes (kind 3)
   DevPool pool[3];              // 0: stage scratch, 1: driver buffers, 2: bdc
   // optional per-kernel-family timing (bench roofline): CUDA events around
   // each launch of a family, with its algorithmic bytes/flops
