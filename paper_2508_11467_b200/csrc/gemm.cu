@@ -85,7 +85,10 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
   const int tid = threadIdx.x;
   // VEC (host-checked: 16-byte aligned bases, even leading dimensions) selects
   // 16-byte cp.async for every pair at compile time.
-  constexpr bool vecA = VEC, vecB = VEC;
+  // GATHER (device descriptors): alignment is known only here, per descriptor
+  // (uniform per CTA): 16-byte copies when the base and leading dimension allow.
+  const bool vecA = VEC || (gather && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && ((lda & 1) == 0));
+  const bool vecB = VEC || (gather && ((reinterpret_cast<uintptr_t>(B) & 15) == 0) && ((ldb & 1) == 0));
 
   auto load_tile = [&](int stage, int kt) {
     const int k0 = kt * BK;
