@@ -357,8 +357,8 @@ __global__ void __launch_bounds__(kPrepThreads) bdc_prep_kernel(const MergeDesc*
                                                                 const double* edge, double* Q, long long ldq,
                                                                 int vectors, double tol_mult, BdcBufs B, int* err) {
   __shared__ double sh_red[32];
-  __shared__ double c_d[kPrepChunk], c_z[kPrepChunk], c_e0[kPrepChunk], c_e1[kPrepChunk];
-  __shared__ unsigned char c_cl[kPrepChunk], c_cr[kPrepChunk];
+  __shared__ int sh_has[kPrepThreads];
+  __shared__ double sh_lastd[kPrepThreads];
   __shared__ int sh_cnt[kPrepThreads][6];
   __shared__ int sh_tot[8];
   const MergeDesc M = merges[blockIdx.x];
@@ -456,108 +456,163 @@ __global__ void __launch_bounds__(kPrepThreads) bdc_prep_kernel(const MergeDesc*
     lmax = fmax(lmax, fmax(fabs(dd), fabs(zz)));
   }
   const double tol = tol_mult * DC_EPS * block_max(lmax, sh_red);
-  // sequential deflation scan (bdc.py:460-498): thread 0 walks chunks staged
-  // in shared memory; the current "last kept" entry p lives in registers.
-  int K = 0, nd = 0, nrot = 0;
-  double pd = 0.0, pz = 0.0, pe0 = 0.0, pe1 = 0.0;
-  int pcl = 0, pcr = 0, pidx = 0;
-  for (int base = 0; base < n; base += kPrepChunk) {
-    const int cnt = min(kPrepChunk, n - base);
-    __syncthreads();
-    for (int t = tid; t < cnt; t += blockDim.x) {
-      const int j = r0 + base + t;
-      c_d[t] = B.dw[j];
-      c_z[t] = B.zw[j];
-      c_e0[t] = B.ew0[j];
-      c_e1[t] = B.ew1[j];
-      c_cl[t] = (unsigned char)B.lcls[j];
-      c_cr[t] = (unsigned char)B.rcls[j];
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int t0 = 0;
-      if (base == 0) {
-        // entry 0: d = 0, z clamp (never deflated)
-        double z = c_z[0];
-        if (fabs(z) <= tol) z = copysign(fmax(tol, DC_TINY), z != 0.0 ? z : 1.0);
-        pd = c_d[0]; pz = z; pe0 = c_e0[0]; pe1 = c_e1[0]; pcl = c_cl[0]; pcr = c_cr[0]; pidx = 0;
-        t0 = 1;
+  // deflation (bdc.py:460-498) by groups.  In the sequential scan a non-tiny
+  // entry j merges into the last kept entry p iff d_j - d_p <= tol, where d_p
+  // is the previous survivor's d (it is copied into p on every merge) except
+  // for p = 0, whose d stays 0.  So on the sorted survivors: the ones with
+  // d <= tol join entry 0's group, any other starts a new group iff it lies
+  // more than tol above the previous survivor.  Entries are classified in
+  // parallel, and one thread walks each group in order (the Givens chain of
+  // a group is sequential; groups are independent), writing outputs at
+  // indices from block-wide prefix counts -- the same results, in the same
+  // order, as the sequential scan.
+  int* ecls = perm;  // reuse per entry: 0 tiny z (deflated), 1 leader (kept), 2 merged into its leader
+  const int T = blockDim.x;
+  const int CH = (n + T - 1) / T;
+  const int c0 = min(n, tid * CH), c1 = min(n, c0 + CH);
+  {
+    int has = 0;
+    double lastd = 0.0;
+    for (int j = c0; j < c1; ++j)
+      if (j == 0 || !(fabs(B.zw[r0 + j]) <= tol)) {
+        has = 1;
+        lastd = B.dw[r0 + j];
       }
-      for (int t = t0; t < cnt; ++t) {
-        const int j = base + t;
-        const double zj = c_z[t];
-        const double dj = c_d[t];
-        if (fabs(zj) <= tol) {
-          B.defl[r0 + nd] = j;
-          B.dval[r0 + nd] = dj;
-          B.dkind[r0 + nd] = 0;
-          B.ew0[r0 + j] = c_e0[t];
-          B.ew1[r0 + j] = c_e1[t];
-          ++nd;
-          continue;
-        }
-        if (dj - pd <= tol) {
-          double c, s, r;
-          lartg(pz, zj, c, s, r);
-          pz = r;
-          B.rot_p[r0 + nrot] = pidx;
-          B.rot_j[r0 + nrot] = j;
-          B.rot_c[r0 + nrot] = c;
-          B.rot_s[r0 + nrot] = s;
-          ++nrot;
-          // edge rows rotate with the right-side columns
-          const double a0 = pe0, b0 = c_e0[t], a1 = pe1, b1 = c_e1[t];
-          pe0 = c * a0 + s * b0;
-          pe1 = c * a1 + s * b1;
-          B.ew0[r0 + j] = c * b0 - s * a0;
-          B.ew1[r0 + j] = c * b1 - s * a1;
-          const int cr = c_cr[t];
-          pcr = (pcr == cr) ? pcr : kMixed;
-          B.defl[r0 + nd] = j;
-          if (pidx == 0) {
-            B.dval[r0 + nd] = 0.0;
-            B.dkind[r0 + nd] = 1;
-          } else {
-            pd = dj;
-            const int cl = c_cl[t];
-            pcl = (pcl == cl) ? pcl : kMixed;
-            B.dval[r0 + nd] = dj;
-            B.dkind[r0 + nd] = 0;
-          }
-          ++nd;
+    sh_has[tid] = has;
+    sh_lastd[tid] = lastd;
+  }
+  __syncthreads();
+  {
+    double prevd = 0.0;  // d of the last survivor before c0 (entry 0 always survives)
+    for (int u = tid - 1; u >= 0; --u)
+      if (sh_has[u]) {
+        prevd = sh_lastd[u];
+        break;
+      }
+    int cnt_t = 0, cnt_l = 0, cnt_m = 0;
+    for (int j = c0; j < c1; ++j) {
+      int cls;
+      if (j == 0) {
+        cls = 1;
+        prevd = 0.0;
+      } else {
+        const double dj = B.dw[r0 + j];
+        if (fabs(B.zw[r0 + j]) <= tol) {
+          cls = 0;
         } else {
-          // finalize p, start a new kept entry
-          B.kept[r0 + K] = pidx;
-          B.ds[r0 + K] = pd;
-          B.zs[r0 + K] = pz;
-          B.kcl[r0 + K] = pcl;
-          B.kcr[r0 + K] = pcr;
-          B.ke0[r0 + K] = pe0;
-          B.ke1[r0 + K] = pe1;
-          ++K;
-          pd = dj; pz = zj; pe0 = c_e0[t]; pe1 = c_e1[t]; pcl = c_cl[t]; pcr = c_cr[t]; pidx = j;
+          cls = (prevd <= tol ? dj > tol : dj - prevd > tol) ? 1 : 2;
+          prevd = dj;
         }
       }
+      ecls[j] = cls;
+      cnt_t += cls == 0;
+      cnt_l += cls == 1;
+      cnt_m += cls == 2;
+    }
+    sh_cnt[tid][0] = cnt_t + cnt_m;  // deflated
+    sh_cnt[tid][1] = cnt_l;          // kept
+    sh_cnt[tid][2] = cnt_m;          // rotations
+  }
+  __syncthreads();
+  if (tid < 3) {  // exclusive prefix over the chunks
+    int run = 0;
+    for (int t = 0; t < T; ++t) {
+      const int v = sh_cnt[t][tid];
+      sh_cnt[t][tid] = run;
+      run += v;
+    }
+    sh_tot[tid] = run;
+  }
+  __syncthreads();
+  {
+    int dix = sh_cnt[tid][0], kix = sh_cnt[tid][1], rix = sh_cnt[tid][2];
+    for (int j = c0; j < c1; ++j) {
+      const int cls = ecls[j];
+      if (cls == 0) {  // tiny z: deflated with its own value, edge entries unchanged
+        B.defl[r0 + dix] = j;
+        B.dval[r0 + dix] = B.dw[r0 + j];
+        B.dkind[r0 + dix] = 0;
+        ++dix;
+        continue;
+      }
+      if (cls == 2) {  // written by its group's walker
+        ++dix;
+        ++rix;
+        continue;
+      }
+      // leader: walk the group (up to the next leader) in scan order
+      double pd = B.dw[r0 + j], pz = B.zw[r0 + j], pe0 = B.ew0[r0 + j], pe1 = B.ew1[r0 + j];
+      int pcl = B.lcls[r0 + j], pcr = B.rcls[r0 + j];
+      if (j == 0 && fabs(pz) <= tol) pz = copysign(fmax(tol, DC_TINY), pz != 0.0 ? pz : 1.0);  // z0 clamp
+      int wd = dix, wr = rix;
+      for (int jb = j + 1; jb < n; jb += 8) {
+        int ec[8];
+        double zq[8], dq[8], e0q[8], e1q[8];
+        int lcq[8], rcq[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {  // loads first: eight entries in flight
+          const int jj = jb + q;
+          ec[q] = jj < n ? ecls[jj] : 1;
+          zq[q] = jj < n ? B.zw[r0 + jj] : 0.0;
+          dq[q] = jj < n ? B.dw[r0 + jj] : 0.0;
+          e0q[q] = jj < n ? B.ew0[r0 + jj] : 0.0;
+          e1q[q] = jj < n ? B.ew1[r0 + jj] : 0.0;
+          lcq[q] = jj < n ? B.lcls[r0 + jj] : 0;
+          rcq[q] = jj < n ? B.rcls[r0 + jj] : 0;
+        }
+        bool stop = false;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (stop) break;
+          const int jj = jb + q;
+          if (ec[q] == 1) {  // next leader (or the end)
+            stop = true;
+            break;
+          }
+          if (ec[q] == 0) {  // tiny entry inside the group: counted, written by its owner
+            ++wd;
+            continue;
+          }
+          double c, sn, r;
+          lartg(pz, zq[q], c, sn, r);
+          pz = r;
+          B.rot_p[r0 + wr] = j;
+          B.rot_j[r0 + wr] = jj;
+          B.rot_c[r0 + wr] = c;
+          B.rot_s[r0 + wr] = sn;
+          ++wr;
+          const double a0 = pe0, b0 = e0q[q], a1 = pe1, b1 = e1q[q];
+          pe0 = c * a0 + sn * b0;
+          pe1 = c * a1 + sn * b1;
+          B.ew0[r0 + jj] = c * b0 - sn * a0;
+          B.ew1[r0 + jj] = c * b1 - sn * a1;
+          pcr = (pcr == rcq[q]) ? pcr : kMixed;
+          B.defl[r0 + wd] = jj;
+          if (j == 0) {  // pairs with the zero pole: right side only, value 0
+            B.dval[r0 + wd] = 0.0;
+            B.dkind[r0 + wd] = 1;
+          } else {
+            pd = dq[q];
+            pcl = (pcl == lcq[q]) ? pcl : kMixed;
+            B.dval[r0 + wd] = dq[q];
+            B.dkind[r0 + wd] = 0;
+          }
+          ++wd;
+        }
+        if (stop) break;
+      }
+      B.kept[r0 + kix] = j;
+      B.ds[r0 + kix] = pd;
+      B.zs[r0 + kix] = pz;
+      B.kcl[r0 + kix] = pcl;
+      B.kcr[r0 + kix] = pcr;
+      B.ke0[r0 + kix] = pe0;
+      B.ke1[r0 + kix] = pe1;
+      ++kix;
     }
   }
   __syncthreads();
-  if (tid == 0) {
-    B.kept[r0 + K] = pidx;
-    B.ds[r0 + K] = pd;
-    B.zs[r0 + K] = pz;
-    B.kcl[r0 + K] = pcl;
-    B.kcr[r0 + K] = pcr;
-    B.ke0[r0 + K] = pe0;
-    B.ke1[r0 + K] = pe1;
-    ++K;
-    sh_tot[0] = K;
-    sh_tot[1] = nd;
-    sh_tot[2] = nrot;
-  }
-  __syncthreads();
-  K = sh_tot[0];
-  nd = sh_tot[1];
-  nrot = sh_tot[2];
+  const int K = sh_tot[1], nd = sh_tot[0], nrot = sh_tot[2];
   // class-ordered positions: W side [F, M, S] over kept k >= 1; Q side [F, M, S]
   {
     const int per = (K + blockDim.x - 1) / blockDim.x;
