@@ -70,7 +70,16 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB)
   constexpr bool gather = GATHER;
   using Cfg = GemmCfg<TA, TB, BM, BN, BK, WARPS_M, WARPS_N, STAGES>;
   constexpr int THREADS = Cfg::THREADS;
-  const GemmDesc& P = ddesc ? ddesc[blockIdx.z] : batch.d[blockIdx.z];
+  const int ks = ddesc ? 1 : batch.ksplit;
+  GemmDesc P = ddesc ? ddesc[blockIdx.z] : batch.d[blockIdx.z / ks];
+  if (ks > 1) {  // split-K slice of this descriptor
+    const int sl = blockIdx.z % ks;
+    const long long k0 = (long long)sl * batch.kchunk;
+    P.k = (int)max(0LL, min((long long)batch.kchunk, (long long)P.k - k0));
+    P.A += TA ? k0 : k0 * P.lda;
+    P.B += TB ? k0 * P.ldb : k0;
+    P.C += sl * batch.cslice;
+  }
   const int M = P.m, N = P.n, K = P.k;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   if (m0 >= M || n0 >= N) return;
@@ -515,7 +524,8 @@ int gemm_launch_batch(cudaStream_t st, bool ta, bool tb, const GemmBatch& b) {
     flops += 2.0 * b.d[i].m * b.d[i].n * b.d[i].k;
   }
   const int sidx = t_cur ? stat_begin(t_cur, 1, flops, st) : -1;
-  const int r = dispatch(st, ta, tb, &b, nullptr, b.count, mm, nn, kk, bnz);
+  const int r = dispatch(st, ta, tb, &b, nullptr, b.count * std::max(1, b.ksplit), mm, nn,
+                         b.ksplit > 1 ? b.kchunk : kk, bnz);
   if (t_cur) stat_end(t_cur, sidx, st);
   return r;
 }

@@ -34,6 +34,11 @@ constexpr int kMaxBatchDesc = 32;
 struct GemmBatch {
   GemmDesc d[kMaxBatchDesc];
   int count;
+  // split-K of every descriptor over blockIdx.z: slice s covers k in
+  // [s*kchunk, (s+1)*kchunk) and writes C + s*cslice (partials for a reduce)
+  int ksplit = 1;
+  int kchunk = 0;
+  long long cslice = 0;
 };
 
 // Host launchers (stream-ordered).  `ta`/`tb` select op(A)=A^T / op(B)=B^T.

@@ -153,11 +153,13 @@ static int grid_for(long long n, int threads = 256) {
 // via cwy_scratch_doubles).
 // Split-K factor for Z = Y^T C (K = rows_y): enough 64x64 tiles x slices for
 // ~3 CTAs per SM, slices of >= 128 rows, partials <= 16M doubles.
+constexpr int kMaxKSplit = 128;  // split-K slices (in-kernel, GemmBatch::ksplit)
+
 static int cwy_split(int sms, int w, long long c_other, long long rows_y) {
   // count 64x128 tiles: enough of them (>= 2 per SM) selects the 2-CTA/SM DMMA config
   const long long zt = ((w + 63) / 64) * ((c_other + 127) / 128);
   int S = 1;
-  while (S < kMaxBatchDesc && zt * S < 2LL * sms && rows_y / (S * 2) >= 256 &&
+  while (S < kMaxKSplit && zt * S < 2LL * sms && rows_y / (S * 2) >= 256 &&
          (long long)(2 * S) * w * c_other <= (16LL << 20))
     S *= 2;
   return S;
@@ -191,34 +193,36 @@ static int cwy_apply(dcsvd_ctx* h, cudaStream_t st, char side, bool trans, bool 
   double* Gp = Zp + (size_t)S * w * c_other;
   double* Top = Gp + (size_t)S * w * w;
   double* TinvT = Top + (size_t)w * w;
-  const long long kchunk = (rows_y + S - 1) / S;
+  // slices of a multiple of 16 rows: every slice base keeps the operands' 16-byte alignment
+  const long long kchunk = (((rows_y + S - 1) / S) + 15) & ~15LL;
+  // one descriptor each, split over K inside the kernel (slice s -> partial s)
   GemmBatch zb, gb;
-  zb.count = 0;
-  gb.count = 0;
-  for (int s = 0; s < S; ++s) {
-    const long long k0 = s * kchunk;
-    const long long kk = std::min(kchunk, rows_y - k0);
+  zb.count = 1;
+  gb.count = 1;
+  zb.ksplit = gb.ksplit = S;
+  zb.kchunk = gb.kchunk = (int)kchunk;
+  zb.cslice = (long long)w * c_other;
+  gb.cslice = (long long)w * w;
+  {
     GemmDesc z, g;
     z.acol = nullptr; z.ccol = nullptr; z.alpha = 1.0; z.beta = 0.0;
     g = z;
-    // op(Y^T) rows k0.. : Y stored normal -> A = Y + k0 (transA); Yt -> A = Yt + k0*ldy
-    const double* Yk = ytrans ? Y + k0 * ldy : Y + k0;
     if (side == 'L') {
-      z.m = w; z.n = (int)c_other; z.k = (int)kk;
-      z.A = Yk; z.lda = ldy;
-      z.B = C + k0; z.ldb = ldc;
-      z.C = Zp + (size_t)s * w * c_other; z.ldc = w;
+      z.m = w; z.n = (int)c_other; z.k = (int)rows_y;
+      z.A = Y; z.lda = ldy;
+      z.B = C; z.ldb = ldc;
+      z.C = Zp; z.ldc = w;
     } else {
-      z.m = (int)c_other; z.n = w; z.k = (int)kk;
-      z.A = C + k0 * ldc; z.lda = ldc;
-      z.B = Yk; z.ldb = ldy;
-      z.C = Zp + (size_t)s * w * c_other; z.ldc = c_other;
+      z.m = (int)c_other; z.n = w; z.k = (int)rows_y;
+      z.A = C; z.lda = ldc;
+      z.B = Y; z.ldb = ldy;
+      z.C = Zp; z.ldc = c_other;
     }
-    g.m = w; g.n = w; g.k = (int)kk;
-    g.A = Yk; g.lda = ldy; g.B = Yk; g.ldb = ldy;
-    g.C = Gp + (size_t)s * w * w; g.ldc = w;
-    zb.d[zb.count++] = z;
-    gb.d[gb.count++] = g;
+    g.m = w; g.n = w; g.k = (int)rows_y;
+    g.A = Y; g.lda = ldy; g.B = Y; g.ldb = ldy;
+    g.C = Gp; g.ldc = w;
+    zb.d[0] = z;
+    gb.d[0] = g;
   }
   int rc;
   if (side == 'L') rc = gemm_launch_batch(st, /*ta=*/!ytrans, /*tb=*/false, zb);
