@@ -112,6 +112,16 @@ __device__ __forceinline__ double warp_allsum(const double* p, int cnt) {
   return warp_sum(((t[0] + t[1]) + (t[2] + t[3])) + t[4]);
 }
 
+// Split form of warp_allsum: issue the loads, reduce later (same order).
+__device__ __forceinline__ void allsum_load(const double* p, int cnt, double (&t)[5]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < 5; ++i) t[i] = lane + 32 * i < cnt ? p[lane + 32 * i] : 0.0;
+}
+__device__ __forceinline__ double allsum_finish(const double (&t)[5]) {
+  return warp_sum(((t[0] + t[1]) + (t[2] + t[3])) + t[4]);
+}
+
 // sum_{t < cnt} x[t * stride] * c[t] with four independent partial chains
 // (fixed combination order -> deterministic).
 __device__ __forceinline__ double dot4(const double* x, long long stride, const double* c, int cnt) {
@@ -548,6 +558,7 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd2_kernel(LabrdArgs a) {
     if (colstep && tid < 2 * k - 1) prow = P[k + (long long)tid * ldp];  // P[k, t], t < 2k-1
     const double yk = k > 0 ? Q[k + (long long)(2 * k - 2) * ldq] : 0.0;  // y_{k-1}[k]
     double pi = 0.0, denr = 1.0, betar = 0.0;
+    tmark(a, 600 + 8 * k + 0);
     if (k > 0) {
       const double alr = a.rvec[k];
       larfg_scalars(alr, warp_allsum(a.normr, a.Gc), pi, betar);
@@ -571,6 +582,7 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd2_kernel(LabrdArgs a) {
         a.taup[k - 1] = pi;
       }
     }
+    tmark(a, 600 + 8 * k + 1);
     // x_{k-1} and c_k for the block rows
     double part = 0.0;
     if (rr < RB) {
@@ -589,6 +601,7 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd2_kernel(LabrdArgs a) {
       sh_c[rr] = (rv && r > k) ? c : 0.0;
     }
     if (colstep && tid < 2 * k - 1) sh_row[tid] = prow;
+    tmark(a, 600 + 8 * k + 2);
     if (!colstep) break;
     part = block_sum(part, sh_red);  // also publishes sh_c / Pc / Qc / sh_row
     if (rowowner && tid == 0) a.normc[gr] = part;
@@ -685,7 +698,9 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd2_kernel(LabrdArgs a) {
     const double xk = k > 0 ? P[k + (long long)(2 * k - 1) * ldp] : 0.0;  // x_{k-1}[k]
     const double alpha = a.cvec[k];
     double tau, beta;
+    tmark(a, 600 + 8 * k + 4);
     larfg_scalars(alpha, warp_allsum(a.normc, a.Gr), tau, beta);
+    tmark(a, 600 + 8 * k + 5);
     const double den = alpha - beta;
     // v_k for the block rows r >= k; owners write P[:, 2k] and column k of A
     if (rr < RB) {
@@ -726,6 +741,7 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd2_kernel(LabrdArgs a) {
       Qc[jj + ty * LQ] = y;
     }
     if (tid < 2 * k) sh_row[tid] = qrow;
+    tmark(a, 600 + 8 * k + 6);
     part = block_sum(part, sh_red);  // also publishes sh_r / Pc / Qc / sh_row
     if (colowner && tid == 0) a.normr[gc] = part;
     tmark(a, tb + 5);
