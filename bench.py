@@ -254,6 +254,32 @@ def run_c4(args, dcs, _lib, torch, dist, ws, rank, local):
     gram.copy_(torch.eye(n, dtype=torch.float64, device=w.device))
     dcs.matmul_accumulate(1.0, w, True, w, False, -1.0, gram)  # W^T W - I with the DMMA GEMM
     orth_w = float(gram.norm().item()) / n
+    # --- e2e: host d/e (pinned) -> bdsdc through the public API -> dvals, W, Q back to pinned host
+    hd = torch.from_numpy(z["d"]).pin_memory()
+    he = torch.from_numpy(z["e"]).pin_memory()
+    out_d = torch.empty(n, dtype=torch.float64).pin_memory()
+    out_w = torch.empty(r.w.numel(), dtype=torch.float64).pin_memory()
+    out_q = torch.empty(r.qfull.numel(), dtype=torch.float64).pin_memory()
+    h2d = (hd.numel() + he.numel()) * 8
+    d2h = (out_d.numel() + out_w.numel() + out_q.numel()) * 8
+
+    def e2e_step():
+        pr = dcs.BidiagonalProblem(hd.to(f"cuda:{local}", non_blocking=True),
+                                   he.to(f"cuda:{local}", non_blocking=True))
+        rr = dcs.bdsdc(pr)
+        out_d.copy_(rr.dvals, non_blocking=True)
+        out_w.copy_(rr.w.t().reshape(-1), non_blocking=True)
+        out_q.copy_(rr.qfull.t().reshape(-1), non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s.record()
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = max(s.elapsed_time(e1), (time.perf_counter() - t0) * 1e3) / args.e2e_steps
     t0 = time.perf_counter()
     rv = dcs.bdsdc(prob, want_vectors=False)
     torch.cuda.synchronize()
@@ -273,6 +299,8 @@ def run_c4(args, dcs, _lib, torch, dist, ws, rank, local):
         "roofline": roof_c4[0],
         "roofline_secondary": roof_c4[1],
         "clocks": clk.summary(),
+        "e2e": {"value": F / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "cpu_baseline": {"value": float(F / float(z["ref_seconds_values_only"]) / 1e9), "unit": "GFLOP/s", "cores": 7,
                          "kind": "reference", "seconds": float(z["ref_seconds_values_only"]),
                          "sample": "reference dcsvd.bdsdc values-only on the same fixture, build container (7 BLAS threads), timed when the fixture was made; with vectors it took 57.2 s (BASELINE.md)"},
