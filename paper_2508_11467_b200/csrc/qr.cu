@@ -288,9 +288,23 @@ struct Geqr2Args {
   double* rowbuf;  // 2 x 64: the pivot row of the current / next column
   unsigned* bar;
   int R1;        // rows per CTA
+  unsigned long long* tlog;
 };
 
 constexpr int kGeqr2Threads = 512;
+constexpr int kGeqr2Warps = kGeqr2Threads / 32;
+static_assert(kGeqr2Warps * 4 >= 64, "four partial slots per warp cover a 64-wide panel");
+extern unsigned long long* g_labrd_tlog;  // debug phase timestamps (gebrd.cu)
+
+// debug: per-CTA timestamps of columns 5 and 6 (4 marks each, 256 slots per mark)
+__device__ __forceinline__ void tmark_g(const Geqr2Args& a, int j, int m) {
+  if (a.tlog && threadIdx.x == 0 && (j == 5 || j == 6)) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.tlog[((j == 6 ? 4 : 0) + m) * 256 + blockIdx.x] = t;
+    a.tlog[(8 + (j == 6 ? 4 : 0) + m) * 256 + blockIdx.x] = clock64();
+  }
+}
 
 // One grid barrier per column.  With v = [1; x/den] (LARFG, densecore.py:
 // 114-128) the reflector's w_t = v^T a[:, t] = a[j, t] + (sum_{r>j} x_r a[r, t]) / den,
@@ -301,7 +315,7 @@ constexpr int kGeqr2Threads = 512;
 __global__ void __launch_bounds__(kGeqr2Threads, 1) geqr2_coop_kernel(Geqr2Args a) {
   extern __shared__ double slab[];  // R1 x w
   __shared__ double sh_w[64];
-  __shared__ double sh_red[32];
+  __shared__ double sh_row[64];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int g = blockIdx.x, G = gridDim.x;
   const int r0 = g * a.R1, r1 = min(a.m, r0 + a.R1), nr = max(0, r1 - r0);
@@ -314,14 +328,16 @@ __global__ void __launch_bounds__(kGeqr2Threads, 1) geqr2_coop_kernel(Geqr2Args 
   __syncthreads();
   // partials of column c over this CTA's rows r > c into buffer (c & 1):
   // slot 0 = sum x^2, slot t = sum x * a[r, t] (t > c); row c published.
+  // Slot-major (part[slot * G + cta]) so one warp reads a slot's G <= 160
+  // partials with five coalesced loads per lane.
   auto partials = [&](int c) {
-    double* part = a.part + (size_t)(c & 1) * G * 64 + (size_t)g * 64;
+    double* part = a.part + (size_t)(c & 1) * G * 64 + g;
     const int lo = max(0, c + 1 - r0);  // first local row > c
     for (int t = c + warp; t < w; t += nw) {  // warp per slot (t == c: the norm)
       double s = 0.0;
       for (int rr = lo + lane; rr < nr; rr += 32) s += slab[rr + c * R1] * slab[rr + t * R1];
       s = warp_sum(s);
-      if (lane == 0) part[t == c ? 0 : t] = s;
+      if (lane == 0) part[(size_t)(t == c ? 0 : t) * G] = s;
     }
     if (c >= r0 && c < r1)
       for (int t = c + tid; t < w; t += blockDim.x) a.rowbuf[(c & 1) * 64 + t] = slab[(c - r0) + t * R1];
@@ -331,16 +347,30 @@ __global__ void __launch_bounds__(kGeqr2Threads, 1) geqr2_coop_kernel(Geqr2Args 
   for (int j = 0; j < w; ++j) {
     const double* part = a.part + (size_t)(j & 1) * G * 64;
     const double* rowj = a.rowbuf + (j & 1) * 64;
-    // reduce the norm (slot 0) and the cross sums (slots j+1..w-1), warp per slot
-    for (int t = j + warp; t < w; t += nw) {
-      const int slot = t == j ? 0 : t;
-      double s = 0.0;
-      for (int i = lane; i < G; i += 32) s += part[(size_t)i * 64 + slot];
-      s = warp_sum(s);
-      if (lane == 0) sh_w[t] = s;
+    // Every load of this column is issued before any is consumed: the
+    // partials of up to four slots per warp (w <= 64, 16 warps) and the
+    // pivot row -- one L2 round trip after the barrier instead of one per
+    // strided load.
+    tmark_g(a, j, 0);
+    double v[4][5];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int t = j + warp + kGeqr2Warps * q;
+      const double* ps = part + (size_t)(t == j ? 0 : t) * G;
+#pragma unroll
+      for (int i = 0; i < 5; ++i) v[q][i] = (t < w && lane + 32 * i < G) ? ps[lane + 32 * i] : 0.0;
     }
+    const double rowv = (tid >= j && tid < w) ? rowj[tid] : 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int t = j + warp + kGeqr2Warps * q;
+      const double s = warp_sum(((v[q][0] + v[q][1]) + (v[q][2] + v[q][3])) + v[q][4]);
+      if (t < w && lane == 0) sh_w[t] = s;
+    }
+    if (tid >= j && tid < w) sh_row[tid] = rowv;
     __syncthreads();
-    const double alpha = rowj[j];
+    tmark_g(a, j, 1);
+    const double alpha = sh_row[j];
     double tau, beta;
     {
       const double xn = sqrt(sh_w[j]);
@@ -350,7 +380,7 @@ __global__ void __launch_bounds__(kGeqr2Threads, 1) geqr2_coop_kernel(Geqr2Args 
     const double den = alpha - beta;
     if (g == 0 && tid == 0) a.tau[j] = tau;
     __syncthreads();  // everyone has read sh_w[j]
-    if (tid > j && tid < w) sh_w[tid] = tau != 0.0 ? rowj[tid] + sh_w[tid] / den : 0.0;  // w_t
+    if (tid > j && tid < w) sh_w[tid] = tau != 0.0 ? sh_row[tid] + sh_w[tid] / den : 0.0;  // w_t
     // column j of the slab: beta on row j, essential part x / den below
     for (int rr = tid; rr < nr; rr += blockDim.x) {
       const int r = r0 + rr;
@@ -370,8 +400,10 @@ __global__ void __launch_bounds__(kGeqr2Threads, 1) geqr2_coop_kernel(Geqr2Args 
       }
       __syncthreads();
     }
+    tmark_g(a, j, 2);
     if (j + 1 < w) {
       partials(j + 1);
+      tmark_g(a, j, 3);
       grid_barrier(a.bar, G, epoch);
     }
   }
@@ -391,6 +423,7 @@ static int geqr2_launch(dcsvd_ctx* h, cudaStream_t st, double* A, long long lda,
   }
   const size_t smem = sizeof(double) * (size_t)R1 * w;
   if (smem > 200 * 1024) return set_error(h, DCSVD_EINVAL, "QR panel too tall for the GPU panel kernel (%d x %d)", m, w);
+  if (G > 160 || w > 64) return set_error(h, DCSVD_EINVAL, "QR panel kernel supports <= 160 CTAs and 64 columns");
   static bool attr = false;
   if (!attr) {
     DC_CUDA_TRY(cudaFuncSetAttribute(geqr2_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -399,7 +432,7 @@ static int geqr2_launch(dcsvd_ctx* h, cudaStream_t st, double* A, long long lda,
   DC_CUDA_TRY(cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned), st));
   Geqr2Args a;
   a.A = A; a.lda = lda; a.m = m; a.w = w; a.tau = tau; a.part = part; a.rowbuf = part + (size_t)2 * G * 64;
-  a.bar = h->d_bar; a.R1 = R1;
+  a.bar = h->d_bar; a.R1 = R1; a.tlog = g_labrd_tlog;
   void* args[] = {&a};
   DC_CUDA_TRY(cudaLaunchCooperativeKernel((void*)geqr2_coop_kernel, dim3(G), dim3(kGeqr2Threads), args, smem, st));
   note_launch();
