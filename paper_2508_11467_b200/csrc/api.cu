@@ -18,6 +18,7 @@
 namespace dc {
 std::atomic<long long> g_launch_count{0};
 extern unsigned long long* g_labrd_tlog;
+extern int g_labrd_gmax;
 extern bool g_labrd_last_two_phase;
 extern int g_gemm_route;
 thread_local dcsvd_ctx* t_cur = nullptr;
@@ -354,6 +355,12 @@ int dcsvd_debug_gemm_route(int mode) {
 }
 
 int dcsvd_debug_labrd_variant(void) { return dc::g_labrd_last_two_phase ? 2 : 4; }
+
+/* cap the LABRD panel grid at gmax CTAs (0 = all SMs; debug / tuning) */
+int dcsvd_debug_labrd_gmax(int gmax) {
+  dc::g_labrd_gmax = gmax;
+  return 0;
+}
 
 int dcsvd_create(dcsvd_handle* out, int device) {
   if (!out) return DCSVD_EINVAL;

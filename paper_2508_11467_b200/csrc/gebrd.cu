@@ -967,10 +967,12 @@ static LabrdWork labrd_work_take(dcsvd_ctx* h, int pool, long long mp, long long
 // One LABRD panel on the mv x nv view Av (bidiag.py:113-165): P (mv x 2nb,
 // ldp) and Q (nv x 2nb, ldq) are zeroed here and filled; only the panel
 // rows/columns of Av change.
+int g_labrd_gmax = 0;  // debug: cap on the LABRD grid (0 = all SMs)
+
 static int labrd_launch(dcsvd_ctx* h, cudaStream_t st, int mv, int nv, double* Av, long long lda, int nb, double* d,
                         double* e, double* tauq, double* taup, double* P, long long ldp, double* Q, long long ldq,
                         const LabrdWork& w) {
-  const int G = h->sms;
+  const int G = g_labrd_gmax > 0 ? std::min(h->sms, g_labrd_gmax) : h->sms;
   DC_CUDA_TRY(cudaMemset2DAsync(P, sizeof(double) * ldp, 0, sizeof(double) * mv, 2 * nb, st));
   DC_CUDA_TRY(cudaMemset2DAsync(Q, sizeof(double) * ldq, 0, sizeof(double) * nv, 2 * nb, st));
   DC_CUDA_TRY(cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned), st));
