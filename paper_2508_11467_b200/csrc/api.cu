@@ -19,6 +19,7 @@ namespace dc {
 std::atomic<long long> g_launch_count{0};
 extern unsigned long long* g_labrd_tlog;
 extern int g_labrd_gmax;
+int set_rankk_prefetch(int on);
 extern bool g_labrd_last_two_phase;
 extern int g_gemm_route;
 thread_local dcsvd_ctx* t_cur = nullptr;
@@ -355,6 +356,9 @@ int dcsvd_debug_gemm_route(int mode) {
 }
 
 int dcsvd_debug_labrd_variant(void) { return dc::g_labrd_last_two_phase ? 2 : 4; }
+
+/* L2 prefetch of the next C tile in the streaming rank-k kernel (debug / tuning) */
+int dcsvd_debug_rankk_prefetch(int on) { return dc::set_rankk_prefetch(on); }
 
 /* cap the LABRD panel grid at gmax CTAs (0 = all SMs; debug / tuning) */
 int dcsvd_debug_labrd_gmax(int gmax) {

@@ -15,6 +15,13 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool val
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+__constant__ int g_rankk_prefetch = 1;
+int set_rankk_prefetch(int on) {  // debug: L2 prefetch of the next C tile in the rank-k kernel
+  return cudaMemcpyToSymbol(g_rankk_prefetch, &on, sizeof(int)) == cudaSuccess ? 0 : -1;
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -393,7 +400,18 @@ __global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P) {
             cv[i][j][h] = (beta != 0.0 && gn < N && gm < M) ? C[(long long)gm + (long long)gn * ldc] : 0.0;
           }
         }
-      if (t + 1 < t1) load_a(buf ^ 1, (t + 1) * MT);
+      if (t + 1 < t1) {
+        load_a(buf ^ 1, (t + 1) * MT);
+        // C lines of the next tile into L2: its register loads at the next
+        // tile's start then return at L2 latency, not HBM latency under load
+        if (beta != 0.0 && g_rankk_prefetch) {
+          constexpr int LINES = MT * 8 / 128;  // 128-byte lines per C column of a tile
+          for (int q = tid; q < NW * LINES; q += THREADS) {
+            const int gn = n0 + q / LINES, gm = (t + 1) * MT + (q % LINES) * 16;
+            if (gn < N && gm < M) prefetch_l2(C + (long long)gm + (long long)gn * ldc);
+          }
+        }
+      }
       cp_async_commit();
       cp_async_wait<1>();
       __syncthreads();
