@@ -312,18 +312,25 @@ __device__ __forceinline__ void tmark_g(const Geqr2Args& a, int j, int m) {
 // same phase, before den is known.  Each CTA keeps its R1-row slab of the
 // panel in shared memory; the owner of row j+1 publishes that row (double
 // buffered, like the partials) for everyone's w.
+// SM = false: panels too tall for shared memory keep each CTA's row slab in
+// place in global memory (same arithmetic, L2-resident for tall-skinny panels).
+template <bool SM>
 __global__ void __launch_bounds__(kGeqr2Threads, 1) geqr2_coop_kernel(Geqr2Args a) {
-  extern __shared__ double slab[];  // R1 x w
+  extern __shared__ double smem_slab[];  // R1 x w when SM
   __shared__ double sh_w[64];
   __shared__ double sh_row[64];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int g = blockIdx.x, G = gridDim.x;
   const int r0 = g * a.R1, r1 = min(a.m, r0 + a.R1), nr = max(0, r1 - r0);
-  const int R1 = a.R1, w = a.w;
+  const int w = a.w;
+  double* slab = SM ? smem_slab : a.A + r0;
+  const long long R1 = SM ? (long long)a.R1 : a.lda;  // slab column stride
   unsigned epoch = 0;
-  for (int idx = tid; idx < nr * w; idx += blockDim.x) {
-    const int rr = idx % nr, t = idx / nr;
-    slab[rr + t * R1] = a.A[(r0 + rr) + (long long)t * a.lda];
+  if (SM) {
+    for (int idx = tid; idx < nr * w; idx += blockDim.x) {
+      const int rr = idx % nr, t = idx / nr;
+      slab[rr + t * R1] = a.A[(r0 + rr) + (long long)t * a.lda];
+    }
   }
   __syncthreads();
   // partials of column c over this CTA's rows r > c into buffer (c & 1):
@@ -407,9 +414,11 @@ __global__ void __launch_bounds__(kGeqr2Threads, 1) geqr2_coop_kernel(Geqr2Args 
       grid_barrier(a.bar, G, epoch);
     }
   }
-  for (int idx = tid; idx < nr * w; idx += blockDim.x) {
-    const int rr = idx % nr, t = idx / nr;
-    a.A[(r0 + rr) + (long long)t * a.lda] = slab[rr + t * R1];
+  if (SM) {
+    for (int idx = tid; idx < nr * w; idx += blockDim.x) {
+      const int rr = idx % nr, t = idx / nr;
+      a.A[(r0 + rr) + (long long)t * a.lda] = slab[rr + t * R1];
+    }
   }
 }
 
@@ -421,12 +430,12 @@ static int geqr2_launch(dcsvd_ctx* h, cudaStream_t st, double* A, long long lda,
     R1 = 32;
     G = (m + R1 - 1) / R1;
   }
-  const size_t smem = sizeof(double) * (size_t)R1 * w;
-  if (smem > 200 * 1024) return set_error(h, DCSVD_EINVAL, "QR panel too tall for the GPU panel kernel (%d x %d)", m, w);
+  const bool in_smem = sizeof(double) * (size_t)R1 * w <= 200 * 1024;
+  const size_t smem = in_smem ? sizeof(double) * (size_t)R1 * w : 0;
   if (G > 160 || w > 64) return set_error(h, DCSVD_EINVAL, "QR panel kernel supports <= 160 CTAs and 64 columns");
   static bool attr = false;
   if (!attr) {
-    DC_CUDA_TRY(cudaFuncSetAttribute(geqr2_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    DC_CUDA_TRY(cudaFuncSetAttribute(geqr2_coop_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
   DC_CUDA_TRY(cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned), st));
@@ -434,7 +443,8 @@ static int geqr2_launch(dcsvd_ctx* h, cudaStream_t st, double* A, long long lda,
   a.A = A; a.lda = lda; a.m = m; a.w = w; a.tau = tau; a.part = part; a.rowbuf = part + (size_t)2 * G * 64;
   a.bar = h->d_bar; a.R1 = R1; a.tlog = g_labrd_tlog;
   void* args[] = {&a};
-  DC_CUDA_TRY(cudaLaunchCooperativeKernel((void*)geqr2_coop_kernel, dim3(G), dim3(kGeqr2Threads), args, smem, st));
+  void* fn = in_smem ? (void*)geqr2_coop_kernel<true> : (void*)geqr2_coop_kernel<false>;
+  DC_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kGeqr2Threads), args, smem, st));
   note_launch();
   return 0;
 }

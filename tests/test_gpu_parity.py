@@ -795,6 +795,20 @@ def test_c3_scale_tall_skinny(cuda):
     _check_report(g, a, r, None, m)
 
 
+@pytest.mark.parametrize("shape", [(400000, 40), (200000, 96), (48, 300000)])
+def test_panels_taller_than_shared_memory(cuda, shape):
+    """Tall-skinny inputs whose QR panel slab per CTA exceeds shared memory
+    (R1 x 32 doubles > 200 KB): the panel kernel keeps the slab in global
+    memory; same accuracy bar as every other shape."""
+    g = _g()
+    m, n = shape
+    spec = g.MatrixSpec("logrand", m, n, 1e6, seed=7)
+    a = g.generate_matrix(spec, device=True)
+    s_ref = g.prescribed_singular_values("logrand", min(m, n), 1e6, seed=7)
+    r = g.gesdd(a)
+    _check_report(g, a, r, s_ref, max(m, n))
+
+
 def test_c5_shaped_batch(cuda):
     """Config C5 shape (2048^2) batch on the concurrent sub-context path."""
     g = _g()
