@@ -19,6 +19,7 @@ namespace dc {
 std::atomic<long long> g_launch_count{0};
 extern unsigned long long* g_labrd_tlog;
 extern int g_labrd_gmax;
+extern int g_gebd2_cluster;
 int set_rankk_prefetch(int on);
 extern bool g_labrd_last_two_phase;
 extern int g_gemm_route;
@@ -356,6 +357,12 @@ int dcsvd_debug_gemm_route(int mode) {
 }
 
 int dcsvd_debug_labrd_variant(void) { return dc::g_labrd_last_two_phase ? 2 : 4; }
+
+/* GEBD2 tail on one thread-block cluster (1, default) or the panel path only (0); debug / A-B */
+int dcsvd_debug_gebd2_cluster(int on) {
+  dc::g_gebd2_cluster = on;
+  return 0;
+}
 
 /* L2 prefetch of the next C tile in the streaming rank-k kernel (debug / tuning) */
 int dcsvd_debug_rankk_prefetch(int on) { return dc::set_rankk_prefetch(on); }

@@ -911,6 +911,263 @@ __global__ void __launch_bounds__(kGebd2Threads) gebd2_kernel(double* A, long lo
 }
 
 // ---------------------------------------------------------------------------
+// GEBD2 on one thread-block cluster (gebrd_unblocked, bidiag.py:75-110) for
+// the trailing block once it fits in the cluster's distributed shared memory
+// (<= ~600 x 600 on 16 SMs).  Each CTA keeps a row slab of the block (all
+// columns) in shared memory; per column the only cross-CTA traffic is DSMEM
+// reads behind four cluster barriers: the column norm partials, the w = A^T v
+// partials (reduce-scatter, then gather) and the row reflector published by
+// the owner of row k.  Replaces the latency-bound panel path at small sizes
+// (two grid barriers plus L2 round trips per column).
+constexpr int kG2cThreads = 512;
+constexpr int kG2cSmemMax = 224 * 1024;
+int g_gebd2_cluster = 1;  // debug: 0 = never use the cluster kernel
+
+struct Gebd2cArgs {
+  double* A;
+  long long lda;
+  int m, n;
+  double *d, *e, *tauq, *taup;
+  int R, LD;  // rows per CTA, slab leading dimension
+  double* ug;  // n: the row reflector u, broadcast through L2 (one source, 16 readers)
+  unsigned long long* tlog;
+};
+
+__global__ void __launch_bounds__(kG2cThreads, 1) gebd2_cluster_kernel(Gebd2cArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int CS = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int m = a.m, n = a.n, R = a.R, LD = a.LD;
+  const int r0 = rank * R, nr = max(0, min(m, r0 + R) - r0);
+  const int S = (n + CS - 1) / CS;  // w slice per CTA
+  int rs = 0;
+  while ((1 << rs) < R) ++rs;
+  const int RP = 1 << rs;  // row lanes of the update loops (R <= 448 < kG2cThreads)
+  extern __shared__ __align__(16) double sm[];
+  double* slab = sm;                      // LD x n: rows r0 .. r0 + nr
+  double* wpart = slab + (size_t)LD * n;  // this CTA's partial w
+  double* wred = wpart + n;               // reduced w, this CTA's slice
+  double* vec = wred + n;                 // local copy of w, then of u
+  double* xr = vec + n;                   // x for own rows
+  __shared__ double sh_red[32];
+  __shared__ double sh_pn, sh_al, sh_pi, sh_s[2];
+  for (int idx = tid; idx < nr * n; idx += blockDim.x) {
+    const int rr = idx % nr, j = idx / nr;
+    slab[rr + (size_t)j * LD] = a.A[(r0 + rr) + (long long)j * a.lda];
+  }
+  __syncthreads();
+  auto mk = [&](int k, int slot) {  // debug: clock64 marks of CTA 0, column 5
+    if (a.tlog && k == 5 && rank == 0 && tid == 0) a.tlog[slot] = clock64();
+  };
+  for (int k = 0; k < n; ++k) {
+    const int ok = k / R;  // CTA owning row k
+    mk(k, 0);
+    // column reflector: partial ||a[k+1:, k]||^2 of own rows
+    double part = 0.0;
+    for (int rr = max(0, k + 1 - r0) + tid; rr < nr; rr += blockDim.x) {
+      const double x = slab[rr + (size_t)k * LD];
+      part += x * x;
+    }
+    part = block_sum(part, sh_red);
+    mk(k, 1);
+    if (tid == 0) {
+      sh_pn = part;
+      if (rank == ok) sh_al = slab[(k - r0) + (size_t)k * LD];
+    }
+    cl.sync();  // #1
+    mk(k, 2);
+    if (warp == 0) {
+      double v = lane < CS ? *cl.map_shared_rank(&sh_pn, lane) : 0.0;
+      v = warp_sum(v);
+      if (lane == 0) {
+        sh_s[0] = v;
+        sh_s[1] = *cl.map_shared_rank(&sh_al, ok);
+      }
+    }
+    __syncthreads();
+    const double alpha = sh_s[1];
+    double tau, beta;
+    larfg_scalars(alpha, sh_s[0], tau, beta);
+    const double den = alpha - beta;
+    if (rank == 0 && tid == 0) {
+      a.tauq[k] = tau;
+      a.d[k] = beta;
+    }
+    for (int rr = max(0, k - r0) + tid; rr < nr; rr += blockDim.x) {
+      if (r0 + rr == k) slab[rr + (size_t)k * LD] = beta;
+      else if (tau != 0.0) slab[rr + (size_t)k * LD] /= den;
+    }
+    __syncthreads();
+    mk(k, 3);
+    const bool left = tau != 0.0 && k + 1 < n;
+    if (left) {  // partial w_j = sum_{own r >= k} v_r a[r, j]
+      const int lo = max(0, k - r0);
+      const double* vk = slab + (size_t)k * LD;
+      for (int j = k + 1 + tid; j < n; j += blockDim.x) {
+        const double* col = slab + (size_t)j * LD;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // four chains, fixed combination order
+        int rr = lo;
+        if (rr < nr && r0 + rr == k) s0 = col[rr++];  // v_k = 1
+        for (; rr + 3 < nr; rr += 4) {
+          s0 = fma(vk[rr], col[rr], s0);
+          s1 = fma(vk[rr + 1], col[rr + 1], s1);
+          s2 = fma(vk[rr + 2], col[rr + 2], s2);
+          s3 = fma(vk[rr + 3], col[rr + 3], s3);
+        }
+        for (; rr < nr; ++rr) s0 = fma(vk[rr], col[rr], s0);
+        wpart[j] = (s0 + s1) + (s2 + s3);
+      }
+    }
+    mk(k, 4);
+    cl.sync();  // #2
+    mk(k, 5);
+    if (left) {  // reduce this CTA's slice of w over the cluster (fixed order)
+      for (int j = max(k + 1, rank * S) + tid; j < min(n, (rank + 1) * S); j += blockDim.x) {
+        double s = 0.0;
+        for (int c = 0; c < CS; ++c) s += cl.map_shared_rank(wpart, c)[j];
+        wred[j] = s;
+      }
+    }
+    mk(k, 6);
+    cl.sync();  // #3
+    mk(k, 7);
+    if (left) {
+      for (int j = k + 1 + tid; j < n; j += blockDim.x) vec[j] = cl.map_shared_rank(wred, j / S)[j];
+      __syncthreads();
+      // thread (row lane, column group): RP = 2^rs >= R row lanes, no divisions
+      const int rr = max(0, k - r0) + (tid & (RP - 1));
+      if (rr < nr) {
+        const double vr = r0 + rr == k ? 1.0 : slab[rr + (size_t)k * LD];
+        for (int j = k + 1 + (tid >> rs); j < n; j += (kG2cThreads >> rs))
+          slab[rr + (size_t)j * LD] -= tau * (vr * vec[j]);
+      }
+    }
+    __syncthreads();
+    mk(k, 8);
+    if (k + 1 >= n) break;
+    // row reflector on a[k, k+1:] (owner of row k), published through L2 (a.ug)
+    if (rank == ok) {
+      const int rk = k - r0;
+      part = 0.0;
+      for (int j = k + 2 + tid; j < n; j += blockDim.x) {
+        const double x = slab[rk + (size_t)j * LD];
+        part += x * x;
+      }
+      part = block_sum(part, sh_red);
+      const double al = slab[rk + (size_t)(k + 1) * LD];
+      double pi, br;
+      larfg_scalars(al, part, pi, br);
+      const double dr = al - br;
+      if (tid == 0) {
+        a.taup[k] = pi;
+        a.e[k] = br;
+        sh_pi = pi;
+        slab[rk + (size_t)(k + 1) * LD] = br;
+      }
+      for (int j = k + 2 + tid; j < n; j += blockDim.x) {
+        double* p = slab + rk + (size_t)j * LD;
+        if (pi != 0.0) *p /= dr;
+        a.ug[j] = *p;
+      }
+      if (tid == 0) a.ug[k + 1] = 1.0;
+    }
+    mk(k, 9);
+    cl.sync();  // #4
+    mk(k, 10);
+    if (tid == 0) sh_s[0] = *cl.map_shared_rank(&sh_pi, ok);
+    __syncthreads();
+    const double pi = sh_s[0];
+    if (pi != 0.0) {
+      for (int j = k + 1 + tid; j < n; j += blockDim.x) vec[j] = __ldcg(a.ug + j);
+      __syncthreads();
+      // x_r = sum_{j>k} a[r, j] u_j for own rows r > k (warp per row), then a -= pi x u^T
+      const int lo = max(0, k + 1 - r0);
+      for (int rr = lo + warp; rr < nr; rr += nw) {
+        double s = 0.0;
+        for (int j = k + 1 + lane; j < n; j += 32) s += slab[rr + (size_t)j * LD] * vec[j];
+        s = warp_sum(s);
+        if (lane == 0) xr[rr] = s;
+      }
+      __syncthreads();
+      const int rr = lo + (tid & (RP - 1));
+      if (rr < nr) {
+        const double xv = xr[rr];
+        for (int j = k + 1 + (tid >> rs); j < n; j += (kG2cThreads >> rs))
+          slab[rr + (size_t)j * LD] -= pi * (xv * vec[j]);
+      }
+    }
+    __syncthreads();
+    mk(k, 11);
+  }
+  if (rank == 0 && tid == 0) a.taup[n - 1] = 0.0;
+  for (int idx = tid; idx < nr * n; idx += blockDim.x) {
+    const int rr = idx % nr, j = idx / nr;
+    a.A[(r0 + rr) + (long long)j * a.lda] = slab[rr + (size_t)j * LD];
+  }
+  cl.sync();  // no CTA exits while its shared memory may still be read
+}
+
+static size_t gebd2c_bytes(int m, int n, int cs, int* R, int* LD) {
+  const int r = (m + cs - 1) / cs, ld = r | 1;  // odd stride: conflict-free column walks
+  if (R) *R = r;
+  if (LD) *LD = ld;
+  return sizeof(double) * ((size_t)ld * n + 4 * (size_t)n + ld);
+}
+
+// cluster size for gebd2_cluster_kernel: 16 when the GPU can co-schedule it, else 8
+static int gebd2c_cluster_size() {
+  static int cs = 0;
+  if (cs) return cs;
+  cudaFuncSetAttribute(gebd2_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kG2cSmemMax);
+  cudaFuncSetAttribute(gebd2_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cs = 8;
+  for (int want : {16}) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = want; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(want); cfg.blockDim = dim3(kG2cThreads); cfg.dynamicSmemBytes = kG2cSmemMax;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, gebd2_cluster_kernel, &cfg) == cudaSuccess && nclusters >= 1)
+      cs = want;
+    cudaGetLastError();
+  }
+  return cs;
+}
+
+// Measured per-column crossover with the two-phase LABRD panels (tools/gebd2_cluster_ab.py):
+// the cluster kernel's work per CTA grows with n^2/16 while the panel path is
+// latency-flat at ~11.5 us per column, so it takes over at n <= 512.
+constexpr int kG2cMaxCols = 512;
+
+static bool gebd2c_fits(int m, int n) {
+  if (!g_gebd2_cluster || n < 64 || n > kG2cMaxCols) return false;
+  return gebd2c_bytes(m, n, gebd2c_cluster_size(), nullptr, nullptr) <= (size_t)kG2cSmemMax;
+}
+
+static int gebd2c_launch(cudaStream_t st, double* A, long long lda, int m, int n, double* d, double* e,
+                         double* tauq, double* taup, double* ug) {
+  const int cs = gebd2c_cluster_size();
+  Gebd2cArgs ga;
+  ga.A = A; ga.lda = lda; ga.m = m; ga.n = n; ga.d = d; ga.e = e; ga.tauq = tauq; ga.taup = taup;
+  ga.ug = ug;
+  ga.tlog = g_labrd_tlog;
+  g_labrd_tlog = nullptr;
+  const size_t smem = gebd2c_bytes(m, n, cs, &ga.R, &ga.LD);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(cs); cfg.blockDim = dim3(kG2cThreads); cfg.dynamicSmemBytes = smem; cfg.stream = st;
+  cfg.attrs = at; cfg.numAttrs = 1;
+  DC_CUDA_TRY(cudaLaunchKernelEx(&cfg, gebd2_cluster_kernel, ga));
+  note_launch();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
 constexpr int kLabrdSmemMax = 225 * 1024;  // 227 KB opt-in minus static shared memory
 
 template <typename K>
@@ -1082,7 +1339,7 @@ int gebrd_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A
   LabrdWork w = labrd_work_take(h, 0, mp, np, G);
   double* wbuf = pool_take<double>(h, 0, mp + np);
   long long off = 0;
-  while (n - off > nb && !unblocked) {
+  while (n - off > nb && !unblocked && !gebd2c_fits((int)(m - off), (int)(n - off))) {
     const int mv = (int)(m - off), nv = (int)(n - off);
     double* Av = A + off + off * lda;
     rc = labrd_launch(h, st, mv, nv, Av, lda, nb, d + off, e + off, tauq + off, taup + off, P, mp, Q, np, w);
@@ -1098,9 +1355,15 @@ int gebrd_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A
     if (rc) return rc;
     off += nb;
   }
-  gebd2_kernel<<<1, kGebd2Threads, 0, st>>>(A + off + off * lda, lda, (int)(m - off), (int)(n - off), d + off,
-                                            e + off, tauq + off, taup + off, wbuf);
-  note_launch();
+  if (gebd2c_fits((int)(m - off), (int)(n - off))) {
+    rc = gebd2c_launch(st, A + off + off * lda, lda, (int)(m - off), (int)(n - off), d + off, e + off, tauq + off,
+                       taup + off, wbuf);
+    if (rc) return rc;
+  } else {
+    gebd2_kernel<<<1, kGebd2Threads, 0, st>>>(A + off + off * lda, lda, (int)(m - off), (int)(n - off), d + off,
+                                              e + off, tauq + off, taup + off, wbuf);
+    note_launch();
+  }
   DC_CUDA_TRY(cudaGetLastError());
   return 0;
 }
