@@ -951,7 +951,7 @@ __global__ void __launch_bounds__(kG2cThreads, 1) gebd2_cluster_kernel(Gebd2cArg
   double* vec = wred + n;                 // local copy of w, then of u
   double* xr = vec + n;                   // x for own rows
   __shared__ double sh_red[32];
-  __shared__ double sh_pn, sh_al, sh_pi, sh_s[2];
+  __shared__ double sh_pn, sh_al, sh_s[2];
   for (int idx = tid; idx < nr * n; idx += blockDim.x) {
     const int rr = idx % nr, j = idx / nr;
     slab[rr + (size_t)j * LD] = a.A[(r0 + rr) + (long long)j * a.lda];
@@ -977,13 +977,12 @@ __global__ void __launch_bounds__(kG2cThreads, 1) gebd2_cluster_kernel(Gebd2cArg
     }
     cl.sync();  // #1
     mk(k, 2);
-    if (warp == 0) {
+    if (warp == 0) {  // the CS norm partials and alpha in one DSMEM round trip
       double v = lane < CS ? *cl.map_shared_rank(&sh_pn, lane) : 0.0;
-      v = warp_sum(v);
-      if (lane == 0) {
-        sh_s[0] = v;
-        sh_s[1] = *cl.map_shared_rank(&sh_al, ok);
-      }
+      const double al = lane == 31 ? *cl.map_shared_rank(&sh_al, ok) : 0.0;
+      v = warp_sum(lane == 31 ? 0.0 : v);
+      if (lane == 0) sh_s[0] = v;
+      if (lane == 31) sh_s[1] = al;
     }
     __syncthreads();
     const double alpha = sh_s[1];
@@ -1062,7 +1061,7 @@ __global__ void __launch_bounds__(kG2cThreads, 1) gebd2_cluster_kernel(Gebd2cArg
       if (tid == 0) {
         a.taup[k] = pi;
         a.e[k] = br;
-        sh_pi = pi;
+        a.ug[k] = pi;  // pi travels with u
         slab[rk + (size_t)(k + 1) * LD] = br;
       }
       for (int j = k + 2 + tid; j < n; j += blockDim.x) {
@@ -1075,12 +1074,10 @@ __global__ void __launch_bounds__(kG2cThreads, 1) gebd2_cluster_kernel(Gebd2cArg
     mk(k, 9);
     cl.sync();  // #4
     mk(k, 10);
-    if (tid == 0) sh_s[0] = *cl.map_shared_rank(&sh_pi, ok);
+    for (int j = k + tid; j < n; j += blockDim.x) vec[j] = __ldcg(a.ug + j);  // pi, then u
     __syncthreads();
-    const double pi = sh_s[0];
+    const double pi = vec[k];
     if (pi != 0.0) {
-      for (int j = k + 1 + tid; j < n; j += blockDim.x) vec[j] = __ldcg(a.ug + j);
-      __syncthreads();
       // x_r = sum_{j>k} a[r, j] u_j for own rows r > k (warp per row), then a -= pi x u^T
       const int lo = max(0, k + 1 - r0);
       for (int rr = lo + warp; rr < nr; rr += nw) {
