@@ -358,7 +358,7 @@ int dcsvd_debug_gemm_route(int mode) {
 
 int dcsvd_debug_labrd_variant(void) { return dc::g_labrd_last_two_phase ? 2 : 4; }
 
-/* GEBD2 tail on one thread-block cluster (1, default) or the panel path only (0); debug / A-B */
+/* GEBD2 tail on one thread-block cluster (1, default; 8 = force 8-CTA clusters) or the panel path only (0); debug */
 int dcsvd_debug_gebd2_cluster(int on) {
   dc::g_gebd2_cluster = on;
   return 0;

@@ -921,7 +921,7 @@ __global__ void __launch_bounds__(kGebd2Threads) gebd2_kernel(double* A, long lo
 // (two grid barriers plus L2 round trips per column).
 constexpr int kG2cThreads = 512;
 constexpr int kG2cSmemMax = 224 * 1024;
-int g_gebd2_cluster = 1;  // debug: 0 = never use the cluster kernel
+int g_gebd2_cluster = 1;  // debug: 0 = never use the cluster kernel, 8 = force 8-CTA clusters
 
 struct Gebd2cArgs {
   double* A;
@@ -1115,6 +1115,7 @@ static size_t gebd2c_bytes(int m, int n, int cs, int* R, int* LD) {
 // cluster size for gebd2_cluster_kernel: 16 when the GPU can co-schedule it, else 8
 static int gebd2c_cluster_size() {
   static int cs = 0;
+  if (g_gebd2_cluster == 8) return 8;  // debug: force the portable cluster size
   if (cs) return cs;
   cudaFuncSetAttribute(gebd2_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kG2cSmemMax);
   cudaFuncSetAttribute(gebd2_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

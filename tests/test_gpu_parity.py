@@ -33,6 +33,12 @@ def _g():
     return g
 
 
+def _lib_handle():
+    from paper_2508_11467_b200 import _lib
+
+    return _lib.load_library()
+
+
 def check_svd(a, sigma, u, vt, sigma_ref):
     m, n = a.shape
     k = min(m, n)
@@ -152,6 +158,37 @@ def test_gebrd_vs_golden(cuda, golden):
         b = np.diag(f.d) + np.diag(f.e, 1)
         sa = np.linalg.svd(golden[f"gebrd{i}_a"], compute_uv=False)
         assert np.max(np.abs(np.linalg.svd(b, compute_uv=False) - sa)) <= 1e-12 * n * sa[0]
+
+
+@pytest.mark.parametrize("mode", [0, 8, 1])
+def test_gebrd_cluster_tail_modes(cuda, golden, mode):
+    """The GEBRD tail on a thread-block cluster (16 CTAs by default, 8 forced)
+    and the panel-only path give the golden factorization (70^2, 64^2 and
+    129x100 run entirely in the cluster kernel; 300x260 switches mid-way)."""
+    g = _g()
+    lib = _lib_handle()
+    lib.dcsvd_debug_gebd2_cluster(mode)
+    try:
+        for i in range(int(golden["gebrd_count"])):
+            a = golden[f"gebrd{i}_a"].copy(order="F")
+            f = g.gebrd_blocked(a, int(golden[f"gebrd{i}_block"]))
+            tol = 1e-13 * a.shape[1] * np.linalg.norm(golden[f"gebrd{i}_a"])
+            assert np.max(np.abs(f.d - golden[f"gebrd{i}_d"])) <= tol
+            assert np.max(np.abs(f.e - golden[f"gebrd{i}_e"])) <= tol
+            assert np.max(np.abs(a - golden[f"gebrd{i}_packed"])) <= tol
+        rng = np.random.default_rng(11)
+        a0 = np.asfortranarray(rng.standard_normal((600, 560)))
+        a = a0.copy(order="F")
+        f = g.gebrd_blocked(a, 32)
+        d, e, tq, tp = oracle.gebd2(a0.copy(order="F"))
+        sc = np.linalg.norm(a0)
+        assert np.max(np.abs(np.abs(f.d) - np.abs(d))) <= 1e-12 * sc
+        assert np.max(np.abs(np.abs(f.e) - np.abs(e))) <= 1e-12 * sc
+        b = np.diag(f.d) + np.diag(f.e, 1)
+        sa = np.linalg.svd(a0, compute_uv=False)
+        assert np.max(np.abs(np.linalg.svd(b, compute_uv=False) - sa)) <= 1e-12 * 560 * sa[0]
+    finally:
+        lib.dcsvd_debug_gebd2_cluster(1)
 
 
 def test_gebrd_unblocked_and_panel(cuda):
@@ -294,6 +331,36 @@ def test_matmul_accumulate(cuda):
     c = np.full((4, 4), np.nan, order="F")
     g.matmul_accumulate(1.0, np.eye(4), False, np.eye(4), False, 0.0, c)  # beta = 0 never reads C
     assert_array_equal(c, np.eye(4))
+
+
+def test_matvec_accumulate(cuda):
+    """densecore.py:96-111 through dcsvd_dgemv: random shapes and both
+    transposes against numpy (test_densecore.py:94-106), beta = 0 never reads
+    y (:108-111), shape mismatch raises (:113-116), plus a long GEMV."""
+    g = _g()
+    rng = np.random.default_rng(7)
+    for _ in range(20):
+        trans_a = bool(rng.integers(0, 2))
+        m, k = (int(v) for v in rng.integers(1, 9, size=2))
+        a = rng.standard_normal((k, m) if trans_a else (m, k))
+        x = rng.standard_normal(k)
+        y = rng.standard_normal(m)
+        alpha, beta = rng.standard_normal(2)
+        expect = beta * y + alpha * ((a.T if trans_a else a) @ x)
+        g.matvec_accumulate(alpha, a, trans_a, x, beta, y)
+        np.testing.assert_allclose(y, expect, rtol=1e-13, atol=1e-13)
+    y = np.full(2, np.nan)
+    g.matvec_accumulate(1.0, np.eye(2), False, np.ones(2), 0.0, y)
+    assert_array_equal(y, np.ones(2))
+    with pytest.raises(ValueError):
+        g.matvec_accumulate(1.0, np.eye(2), False, np.zeros(3), 0.0, np.zeros(2))
+    for trans_a in (False, True):
+        a = np.asfortranarray(rng.standard_normal((3000, 700)))
+        x = rng.standard_normal(3000 if trans_a else 700)
+        y = rng.standard_normal(700 if trans_a else 3000)
+        expect = 0.25 * y - 1.5 * ((a.T if trans_a else a) @ x)
+        g.matvec_accumulate(-1.5, a, trans_a, x, 0.25, y)
+        assert np.max(np.abs(y - expect)) <= 1e-13 * 3000 * np.max(np.abs(expect))
 
 
 def test_gesdd_batched(cuda):

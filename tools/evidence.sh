@@ -11,4 +11,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/la
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -k regex:labrd4 -c 1 -o $O/labrd4_full python tools/prof_svd.py 8192 8192 1 > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -k regex:labrd2 -c 1 -o $O/labrd2_full python tools/prof_svd.py 2048 2048 1 > /dev/null 2>&1
+ncu --set full --import-source on --clock-control none -k regex:gebd2_cluster -c 1 -o $O/gebd2c_full python tools/prof_svd.py 1024 1024 1 > /dev/null 2>&1
 ls -la $O
