@@ -263,7 +263,7 @@ int gesdd_tall(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* 
   const bool vec = o.want_vectors != 0;
   const bool ts = (double)m >= o.ts_crossover * (double)n && m > n;
   size_t need = pool_bytes(4 * n + 8, 8);
-  if (ts) need += pool_bytes(n, 8) + pool_bytes((size_t)n * n, 8) + (vec ? pool_bytes((size_t)n * n, 8) + pool_bytes((size_t)m * n, 8) : 0);
+  if (ts) need += pool_bytes(n, 8) + pool_bytes((size_t)n * n, 8);
   int rc = pool_reserve(h, 1, need, st);
   if (rc) return rc;
   double* dbuf = pool_take<double>(h, 1, 4 * n + 8);
@@ -271,26 +271,21 @@ int gesdd_tall(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* 
   // TS path (driver.py:132-143)
   double* tau = pool_take<double>(h, 1, n);
   double* R = pool_take<double>(h, 1, (size_t)n * n);
-  double* U0 = vec ? pool_take<double>(h, 1, (size_t)n * n) : nullptr;
-  double* Qm = vec ? pool_take<double>(h, 1, (size_t)m * n) : nullptr;
   pt.mark(PH_GEQRF);
   rc = geqrf_run(h, st, m, n, A, lda, tau, o.qr_block);
   if (rc) return rc;
   triu_copy_kernel<<<std::min<long long>(148 * 8, (n * n + 255) / 256), 256, 0, st>>>((int)n, A, lda, R, n);
   note_launch();
-  rc = square_core(h, st, n, n, R, n, S, U0, n, VT, ldvt, o, pt, dbuf);
+  // the core SVD of R writes its left vectors U0 straight into the top n rows of U
+  rc = square_core(h, st, n, n, R, n, S, vec ? U : nullptr, ldu, VT, ldvt, o, pt, dbuf);
   if (rc || !vec) return rc;
-  pt.mark(PH_ORGQR);
-  rc = orgqr_run(h, st, m, n, n, A, lda, tau, Qm, m, kDriverCwyWidth);
-  if (rc) return rc;
+  // Recombination U = Q [U0; 0] (driver.py:141-142 forms Q = orgqr(...) and
+  // multiplies): applying the n QR reflectors to [U0; 0] in 128-wide CWY
+  // blocks is the same product with 4mn^2 - 2n^3 flops instead of
+  // 4mn^2 - 4n^3/3 (ORGQR) + 2mn^2 (GEMM), and needs no m x n Q.
   pt.mark(PH_GEMM);
-  GemmDesc g;
-  g.m = (int)m; g.n = (int)n; g.k = (int)n;
-  g.A = Qm; g.lda = m; g.acol = nullptr;
-  g.B = U0; g.ldb = n;
-  g.C = U; g.ldc = ldu; g.ccol = nullptr;
-  g.alpha = 1.0; g.beta = 0.0;
-  return gemm_launch(st, false, false, g);
+  if (m > n) DC_CUDA_TRY(cudaMemset2DAsync(U + n, sizeof(double) * ldu, 0, sizeof(double) * (m - n), n, st));
+  return ormbr_run(h, st, 'Q', false, m, n, A, lda, tau, U, m, n, ldu, kDriverCwyWidth);
 }
 
 int validate_opts(dcsvd_ctx* h, const dcsvd_opts& o) {
