@@ -1114,24 +1114,23 @@ static size_t gebd2c_bytes(int m, int n, int cs, int* R, int* LD) {
 
 // cluster size for gebd2_cluster_kernel: 16 when the GPU can co-schedule it, else 8
 static int gebd2c_cluster_size() {
-  static int cs = 0;
   if (g_gebd2_cluster == 8) return 8;  // debug: force the portable cluster size
-  if (cs) return cs;
-  cudaFuncSetAttribute(gebd2_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kG2cSmemMax);
-  cudaFuncSetAttribute(gebd2_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  cs = 8;
-  for (int want : {16}) {
+  // thread-safe one-time probe (batched SVDs call this from several host threads)
+  static const int cs = [] {
+    cudaFuncSetAttribute(gebd2_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kG2cSmemMax);
+    cudaFuncSetAttribute(gebd2_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = want; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(want); cfg.blockDim = dim3(kG2cThreads); cfg.dynamicSmemBytes = kG2cSmemMax;
+    at[0].val.clusterDim.x = 16; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(16); cfg.blockDim = dim3(kG2cThreads); cfg.dynamicSmemBytes = kG2cSmemMax;
     cfg.attrs = at; cfg.numAttrs = 1;
     int nclusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclusters, gebd2_cluster_kernel, &cfg) == cudaSuccess && nclusters >= 1)
-      cs = want;
+    const bool ok16 = cudaOccupancyMaxActiveClusters(&nclusters, gebd2_cluster_kernel, &cfg) == cudaSuccess &&
+                      nclusters >= 1;
     cudaGetLastError();
-  }
+    return ok16 ? 16 : 8;
+  }();
   return cs;
 }
 
