@@ -624,6 +624,8 @@ static void free_ctx_resources(dcsvd_ctx* h) {
   }
   for (auto& p : h->pool)
     if (p.ptr) cudaFree(p.ptr);
+  if (h->h_stage) cudaFreeHost(h->h_stage);
+  if (h->ev_stage) cudaEventDestroy(h->ev_stage);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   cudaFree(h->d_err);
   cudaFree(h->d_bar);

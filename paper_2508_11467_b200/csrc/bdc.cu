@@ -33,6 +33,7 @@
 #include <algorithm>
 #include <vector>
 
+#include <cstring>
 #include "ctx.cuh"
 #include "gemm.cuh"
 #include "launch.cuh"
@@ -1284,13 +1285,34 @@ int bdsdc_run(dcsvd_ctx* h, cudaStream_t st, long long n_, const double* d, cons
     for (auto& m : levels[lv]) flat.push_back(m);
   }
   level_off[H + 1] = (int)flat.size();
-  DC_CUDA_TRY(cudaMemcpyAsync(d_leaves, leaves.data(), leaves.size() * sizeof(LeafDesc), cudaMemcpyHostToDevice, st));
-  if (!flat.empty())
-    DC_CUDA_TRY(cudaMemcpyAsync(d_merges, flat.data(), flat.size() * sizeof(MergeDesc), cudaMemcpyHostToDevice, st));
-  if (!unit_rows.empty())
-    DC_CUDA_TRY(cudaMemcpyAsync(d_units, unit_rows.data(), unit_rows.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-  // The host vectors must outlive the async copies: synchronize here (tiny).
-  DC_CUDA_TRY(cudaStreamSynchronize(st));
+  // Through the handle's pinned staging buffer: the copies stay asynchronous
+  // (no stream drain, so the host builds the next call's tree while the GPU
+  // still runs this one); only a previous upload from the same buffer is
+  // waited for before it is overwritten.
+  {
+    const size_t b_leaves = leaves.size() * sizeof(LeafDesc), b_flat = flat.size() * sizeof(MergeDesc),
+                 b_units = unit_rows.size() * sizeof(int);
+    const size_t o_flat = (b_leaves + 255) & ~size_t(255), o_units = o_flat + ((b_flat + 255) & ~size_t(255));
+    const size_t need = o_units + b_units + 256;
+    if (h->stage_pending) DC_CUDA_TRY(cudaEventSynchronize(h->ev_stage));
+    h->stage_pending = false;
+    if (!h->ev_stage) DC_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_stage, cudaEventDisableTiming));
+    if (h->h_stage_bytes < need) {
+      if (h->h_stage) cudaFreeHost(h->h_stage);
+      h->h_stage = nullptr;
+      h->h_stage_bytes = 0;
+      DC_CUDA_TRY(cudaMallocHost(&h->h_stage, need * 2));
+      h->h_stage_bytes = need * 2;
+    }
+    memcpy(h->h_stage, leaves.data(), b_leaves);
+    if (b_flat) memcpy(h->h_stage + o_flat, flat.data(), b_flat);
+    if (b_units) memcpy(h->h_stage + o_units, unit_rows.data(), b_units);
+    DC_CUDA_TRY(cudaMemcpyAsync(d_leaves, h->h_stage, b_leaves, cudaMemcpyHostToDevice, st));
+    if (b_flat) DC_CUDA_TRY(cudaMemcpyAsync(d_merges, h->h_stage + o_flat, b_flat, cudaMemcpyHostToDevice, st));
+    if (b_units) DC_CUDA_TRY(cudaMemcpyAsync(d_units, h->h_stage + o_units, b_units, cudaMemcpyHostToDevice, st));
+    DC_CUDA_TRY(cudaEventRecord(h->ev_stage, st));
+    h->stage_pending = true;
+  }
   if (vectors) {
     DC_CUDA_TRY(cudaMemsetAsync(W, 0, mat * sizeof(double), st));
     DC_CUDA_TRY(cudaMemsetAsync(Q, 0, mat * sizeof(double), st));

@@ -39,6 +39,12 @@ struct dcsvd_ctx {
   std::vector<StatRec> stats;
   std::vector<cudaEvent_t> ev_free;  // recycled timing events (no create/destroy per launch)
   cudaEvent_t ev_stats0 = nullptr;    // recorded when stats are (re)enabled: time origin of the records
+  // pinned staging for small host->device uploads (BDC tree descriptors): the
+  // copies stay asynchronous; ev_stage guards reuse of the buffer
+  char* h_stage = nullptr;
+  size_t h_stage_bytes = 0;
+  cudaEvent_t ev_stage = nullptr;
+  bool stage_pending = false;
 };
 
 namespace dc {
