@@ -19,6 +19,7 @@ namespace dc {
 std::atomic<long long> g_launch_count{0};
 extern unsigned long long* g_labrd_tlog;
 extern int g_labrd_gmax;
+extern double g_labrd_l2keep;
 extern int g_gebd2_cluster;
 int set_rankk_prefetch(int on);
 extern bool g_labrd_last_two_phase;
@@ -361,6 +362,12 @@ int dcsvd_debug_gebd2_cluster(int on) {
 
 /* L2 prefetch of the next C tile in the streaming rank-k kernel (debug / tuning) */
 int dcsvd_debug_rankk_prefetch(int on) { return dc::set_rankk_prefetch(on); }
+
+/* L2 bytes of each large-panel GEMV pass loaded evict_last (0 = plain loads; debug / tuning) */
+int dcsvd_debug_labrd_l2keep(double bytes) {
+  dc::g_labrd_l2keep = bytes;
+  return 0;
+}
 
 /* cap the LABRD panel grid at gmax CTAs (0 = all SMs; debug / tuning) */
 int dcsvd_debug_labrd_gmax(int gmax) {

@@ -45,7 +45,23 @@ struct LabrdArgs {
   int R1, C1;                // 1-D slices (labrd4_kernel)
   unsigned long long* tlog;  // optional phase timestamps (CTA 0, thread 0)
   int cache_pq;              // labrd4_kernel: P/Q 1-D slices cached in shared memory
+  double l2keep;             // labrd4_kernel: bytes of each GEMV pass's tail kept in L2 (evict_last), 0 = plain loads
 };
+
+// L2 eviction-priority loads for the GEMV passes: the tail of each pass (read
+// first by the next, snake-ordered pass) is loaded evict_last, the rest
+// evict_first, so the streamed head cannot push the reusable tail out of L2.
+__device__ __forceinline__ unsigned long long l2_policy(bool keep) {
+  unsigned long long p;
+  if (keep) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ld_l2hint(const double* ptr, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(ptr), "l"(pol));
+  return v;
+}
 
 unsigned long long* g_labrd_tlog = nullptr;  // debug: set by dcsvd_debug_labrd_tlog
 bool g_labrd_last_two_phase = false;          // debug: variant of the last launch
@@ -154,7 +170,7 @@ __device__ __forceinline__ void larfg_scalars(double alpha, double nrm2, double&
 // slice): every entry of those slices is produced by this CTA (row/column
 // ownership is the same in every phase), so the per-row / per-column
 // corrections never touch global P/Q for them.
-template <int RPL>
+template <int RPL, bool HINT>
 __global__ void __launch_bounds__(kLabrdThreads, 1) labrd4_kernel(LabrdArgs a) {
   extern __shared__ double dsm[];
   __shared__ double sh_red[32];
@@ -256,18 +272,35 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd4_kernel(LabrdArgs a) {
         v[i] = (r == k) ? 1.0 : (r > k ? v[i] / den : 0.0);
       }
       const int jstart = max(bc0, k + 1);
+      // columns >= jkeep (this block's tail of the pass) are kept in L2 for the A u pass
+      const double pass_bytes = 8.0 * (double)(a.m - k) * (double)(a.n - k - 1);
+      const double fkeep = a.l2keep > 0.0 ? fmin(1.0, a.l2keep / fmax(pass_bytes, 1.0)) : 1.0;
+      const int jkeep = bc1 - (int)ceil(fkeep * (double)max(0, bc1 - jstart));
+      const unsigned long long pol_keep = HINT ? l2_policy(true) : 0ull, pol_drop = HINT ? l2_policy(false) : 0ull;
       for (int j = jstart + warp; j < bc1; j += 2 * kLabrdWarps) {
         const int j2 = j + kLabrdWarps;
         const bool has2 = j2 < bc1;
         const double* col0 = A + (long long)j * lda;
         const double* col1 = A + (long long)(has2 ? j2 : j) * lda;
         double x0[RPL], x1[RPL];
+        if (HINT) {
+          const unsigned long long p0 = j >= jkeep ? pol_keep : pol_drop;
+          const unsigned long long p1 = (has2 ? j2 : j) >= jkeep ? pol_keep : pol_drop;
 #pragma unroll
-        for (int i = 0; i < RPL; ++i) {
-          const int r = br0 + lane + 32 * i;
-          const bool ok = r < br1;
-          x0[i] = ok ? col0[r] : 0.0;
-          x1[i] = ok ? col1[r] : 0.0;
+          for (int i = 0; i < RPL; ++i) {
+            const int r = br0 + lane + 32 * i;
+            const bool ok = r < br1;
+            x0[i] = ok ? ld_l2hint(col0 + r, p0) : 0.0;
+            x1[i] = ok ? ld_l2hint(col1 + r, p1) : 0.0;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) {
+            const int r = br0 + lane + 32 * i;
+            const bool ok = r < br1;
+            x0[i] = ok ? col0[r] : 0.0;
+            x1[i] = ok ? col1[r] : 0.0;
+          }
         }
         double s0 = 0.0, s1 = 0.0;
 #pragma unroll
@@ -385,6 +418,11 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd4_kernel(LabrdArgs a) {
       for (int i = 0; i < RPL; ++i) acc[i] = 0.0;
       // descending column order (snake against the A^T v pass), 2 columns per step
       const int nj = bc1 - jlo;
+      // this pass ends on the lowest columns: keep those (jj < nkeep) for the next column's A^T v pass
+      const double pass_bytes = 8.0 * (double)(a.m - k - 1) * (double)(a.n - k - 1);
+      const double fkeep = a.l2keep > 0.0 ? fmin(1.0, a.l2keep / fmax(pass_bytes, 1.0)) : 1.0;
+      const int nkeep = (int)ceil(fkeep * (double)max(0, nj));
+      const unsigned long long pol_keep = HINT ? l2_policy(true) : 0ull, pol_drop = HINT ? l2_policy(false) : 0ull;
       for (int jj = nj - 1 - warp; jj >= 0; jj -= 2 * kLabrdWarps) {
         const int j = jlo + jj;
         const int jj2 = jj - kLabrdWarps;
@@ -395,12 +433,24 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd4_kernel(LabrdArgs a) {
         const double* col0 = A + (long long)j * lda;
         const double* col1 = A + (long long)j2 * lda;
         double x0[RPL], x1[RPL];
+        if (HINT) {
+          const unsigned long long p0 = jj < nkeep ? pol_keep : pol_drop;
+          const unsigned long long p1 = (has2 ? jj2 : jj) < nkeep ? pol_keep : pol_drop;
 #pragma unroll
-        for (int i = 0; i < RPL; ++i) {
-          const int r = br0 + lane + 32 * i;
-          const bool ok = r < br1;
-          x0[i] = ok ? col0[r] : 0.0;
-          x1[i] = ok ? col1[r] : 0.0;
+          for (int i = 0; i < RPL; ++i) {
+            const int r = br0 + lane + 32 * i;
+            const bool ok = r < br1;
+            x0[i] = ok ? ld_l2hint(col0 + r, p0) : 0.0;
+            x1[i] = ok ? ld_l2hint(col1 + r, p1) : 0.0;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) {
+            const int r = br0 + lane + 32 * i;
+            const bool ok = r < br1;
+            x0[i] = ok ? col0[r] : 0.0;
+            x1[i] = ok ? col1[r] : 0.0;
+          }
         }
 #pragma unroll
         for (int i = 0; i < RPL; ++i) acc[i] += x0[i] * u0 + x1[i] * u1;
@@ -1186,10 +1236,14 @@ static int launch_labrd(cudaStream_t st, LabrdArgs& la, int grid, size_t smem, b
     }
   }
   switch (rpl) {
-    case 2: return launch_coop(labrd4_kernel<2>, st, la, grid, smem);
-    case 4: return launch_coop(labrd4_kernel<4>, st, la, grid, smem);
-    case 8: return launch_coop(labrd4_kernel<8>, st, la, grid, smem);
-    default: return launch_coop(labrd4_kernel<16>, st, la, grid, smem);
+    case 2: return la.l2keep > 0.0 ? launch_coop(labrd4_kernel<2, true>, st, la, grid, smem)
+                                   : launch_coop(labrd4_kernel<2, false>, st, la, grid, smem);
+    case 4: return la.l2keep > 0.0 ? launch_coop(labrd4_kernel<4, true>, st, la, grid, smem)
+                                   : launch_coop(labrd4_kernel<4, false>, st, la, grid, smem);
+    case 8: return la.l2keep > 0.0 ? launch_coop(labrd4_kernel<8, true>, st, la, grid, smem)
+                                   : launch_coop(labrd4_kernel<8, false>, st, la, grid, smem);
+    default: return la.l2keep > 0.0 ? launch_coop(labrd4_kernel<16, true>, st, la, grid, smem)
+                                    : launch_coop(labrd4_kernel<16, false>, st, la, grid, smem);
   }
 }
 
@@ -1222,6 +1276,9 @@ static LabrdWork labrd_work_take(dcsvd_ctx* h, int pool, long long mp, long long
 // ldp) and Q (nv x 2nb, ldq) are zeroed here and filled; only the panel
 // rows/columns of Av change.
 int g_labrd_gmax = 0;  // debug: cap on the LABRD grid (0 = all SMs)
+// bytes of each large-panel GEMV pass kept in L2 with evict_last, the rest evict_first
+// (tools/labrd_l2keep_ab.py at 8192^2: GEBRD 539 -> 532 ms for 16-24 MB; 64+ MB is slower)
+double g_labrd_l2keep = 20.0 * (1 << 20);
 
 static int labrd_launch(dcsvd_ctx* h, cudaStream_t st, int mv, int nv, double* Av, long long lda, int nb, double* d,
                         double* e, double* tauq, double* taup, double* P, long long ldp, double* Q, long long ldq,
@@ -1239,6 +1296,7 @@ static int labrd_launch(dcsvd_ctx* h, cudaStream_t st, int mv, int nv, double* A
   la.bar = h->d_bar;
   la.tlog = g_labrd_tlog;
   g_labrd_tlog = nullptr;  // log one launch only
+  la.l2keep = g_labrd_l2keep;
   // 2-D geometry for rows-per-lane rpl: Gr x Gc <= G blocks of RB x CB
   auto geom = [&](int rpl, int& Gr, int& Gc, int& CB) {
     const int RB = 32 * rpl;
