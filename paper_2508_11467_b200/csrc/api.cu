@@ -20,6 +20,7 @@ std::atomic<long long> g_launch_count{0};
 extern unsigned long long* g_labrd_tlog;
 extern int g_labrd_gmax;
 extern double g_labrd_l2keep;
+extern double g_labrd_l2keep_min;
 extern int g_gebd2_cluster;
 int set_rankk_prefetch(int on);
 extern bool g_labrd_last_two_phase;
@@ -366,6 +367,12 @@ int dcsvd_debug_rankk_prefetch(int on) { return dc::set_rankk_prefetch(on); }
 /* L2 bytes of each large-panel GEMV pass loaded evict_last (0 = plain loads; debug / tuning) */
 int dcsvd_debug_labrd_l2keep(double bytes) {
   dc::g_labrd_l2keep = bytes;
+  return 0;
+}
+
+/* smallest panel matrix (bytes) that uses the L2 hints (debug / tuning) */
+int dcsvd_debug_labrd_l2keep_min(double bytes) {
+  dc::g_labrd_l2keep_min = bytes;
   return 0;
 }
 

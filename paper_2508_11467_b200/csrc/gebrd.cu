@@ -1279,6 +1279,7 @@ int g_labrd_gmax = 0;  // debug: cap on the LABRD grid (0 = all SMs)
 // bytes of each large-panel GEMV pass kept in L2 with evict_last, the rest evict_first
 // (tools/labrd_l2keep_ab.py at 8192^2: GEBRD 539 -> 532 ms for 16-24 MB; 64+ MB is slower)
 double g_labrd_l2keep = 20.0 * (1 << 20);
+double g_labrd_l2keep_min = 160.0 * (1 << 20);  // panels whose matrix is smaller use plain loads (n' < ~4600)
 
 static int labrd_launch(dcsvd_ctx* h, cudaStream_t st, int mv, int nv, double* Av, long long lda, int nb, double* d,
                         double* e, double* tauq, double* taup, double* P, long long ldp, double* Q, long long ldq,
@@ -1296,7 +1297,9 @@ static int labrd_launch(dcsvd_ctx* h, cudaStream_t st, int mv, int nv, double* A
   la.bar = h->d_bar;
   la.tlog = g_labrd_tlog;
   g_labrd_tlog = nullptr;  // log one launch only
-  la.l2keep = g_labrd_l2keep;
+  // only where the panel's matrix is several times the L2: at 3072^2-4096^2 the
+  // hinted loads are slower than plain ones (tools/labrd_l2keep_ab.py)
+  la.l2keep = 8.0 * (double)mv * (double)nv > g_labrd_l2keep_min ? g_labrd_l2keep : 0.0;
   // 2-D geometry for rows-per-lane rpl: Gr x Gc <= G blocks of RB x CB
   auto geom = [&](int rpl, int& Gr, int& Gc, int& CB) {
     const int RB = 32 * rpl;

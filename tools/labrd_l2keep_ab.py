@@ -10,6 +10,9 @@ import paper_2508_11467_b200 as g
 from paper_2508_11467_b200 import _lib
 lib = _lib.load_library()
 lib.dcsvd_debug_labrd_l2keep.argtypes = [ctypes.c_double]
+lib.dcsvd_debug_labrd_l2keep_min.argtypes = [ctypes.c_double]
+if os.environ.get("L2KEEP_MIN_MB"):
+    lib.dcsvd_debug_labrd_l2keep_min(float(os.environ["L2KEEP_MIN_MB"]) * 2**20)
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 mbs = [float(x) for x in sys.argv[2:]] or [0, 48, 64, 80, 96]
 a = torch.rand(n, n, dtype=torch.float64, device="cuda").t()
