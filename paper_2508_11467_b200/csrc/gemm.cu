@@ -1,4 +1,8 @@
 // DMMA GEMM kernels (see gemm.cuh).
+#include <algorithm>
+#include <unordered_map>
+#include <vector>
+
 #include "ctx.cuh"
 #include "gemm.cuh"
 #include "launch.cuh"
@@ -322,11 +326,11 @@ struct RankkCfg {
   static constexpr int LDA_S = MT + 4;
   static constexpr int A_ELEMS = KMAX * (MT + 4);
   static constexpr int SMEM_BYTES = (B_ELEMS + 2 * A_ELEMS) * 8;
-  static constexpr int CHUNK = 8;  // row tiles per work unit
+  static constexpr int CHUNK = 8;  // most row tiles per work unit (B strip reuse)
 };
 
 template <bool TB, int KMAX, int MT, int WARPS_M, bool VEC>
-__global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P) {
+__global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P, int chunk) {
   using Cfg = RankkCfg<TB, KMAX, MT, WARPS_M>;
   constexpr int THREADS = Cfg::THREADS, NW = Cfg::NW;
   extern __shared__ __align__(16) double smem[];
@@ -344,7 +348,7 @@ __global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P) {
   const int Kp = (K + 3) & ~3;
   const int strips = (N + NW - 1) / NW;
   const int tiles = (M + MT - 1) / MT;
-  const int chunks = (tiles + Cfg::CHUNK - 1) / Cfg::CHUNK;
+  const int chunks = (tiles + chunk - 1) / chunk;
   const int units = strips * chunks;
 
   auto load_a = [&](int buf, int m0) {
@@ -364,7 +368,7 @@ __global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P) {
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int s = u / chunks, ch = u % chunks;
     const int n0 = s * NW;
-    const int t0 = ch * Cfg::CHUNK, t1 = min(tiles, t0 + Cfg::CHUNK);
+    const int t0 = ch * chunk, t1 = min(tiles, t0 + chunk);
     if (TB) {
       for (int p = tid; p < Kp * NW / 2; p += THREADS) {  // B[n + k*ldb]: pairs along n
         const int j = 2 * (p % (NW / 2)), kk = p / (NW / 2);
@@ -404,12 +408,16 @@ __global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P) {
         load_a(buf ^ 1, (t + 1) * MT);
         // C lines of the next tile into L2: its register loads at the next
         // tile's start then return at L2 latency, not HBM latency under load
-        if (beta != 0.0 && g_rankk_prefetch) {
+        // (g_rankk_prefetch = how many tiles ahead; the unit's first tile
+        // also covers the tiles before that distance)
+        const int dist = g_rankk_prefetch;
+        if (beta != 0.0 && dist > 0) {
           constexpr int LINES = MT * 8 / 128;  // 128-byte lines per C column of a tile
-          for (int q = tid; q < NW * LINES; q += THREADS) {
-            const int gn = n0 + q / LINES, gm = (t + 1) * MT + (q % LINES) * 16;
-            if (gn < N && gm < M) prefetch_l2(C + (long long)gm + (long long)gn * ldc);
-          }
+          for (int d = (t == t0 ? 1 : dist); d <= dist && t + d < t1; ++d)
+            for (int q = tid; q < NW * LINES; q += THREADS) {
+              const int gn = n0 + q / LINES, gm = (t + d) * MT + (q % LINES) * 16;
+              if (gn < N && gm < M) prefetch_l2(C + (long long)gm + (long long)gn * ldc);
+            }
         }
       }
       cp_async_commit();
@@ -457,6 +465,57 @@ __global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P) {
   }
 }
 
+// Row tiles per work unit.  The CTAs take units round-robin, so the kernel's
+// time is the largest per-CTA sum of unit costs: the unit's rows in tiles
+// (the last tile may be short) plus a fixed start cost `s` for loading its B
+// strip (measured: s ~ 0.05 tile for the K = 64 / 128-row config, ~0.25 for
+// the K = 128 / 64-row one, i.e. s = KMAX / (8 MT)).  Candidates CHUNK,
+// CHUNK/2, ..., 1; the largest within 2 % of the best makespan wins (large
+// trailing matrices keep 8-tile units, small ones get short units that fill
+// the 148 SMs).  g_rankk_chunk > 0 forces it (debug).
+static int g_rankk_chunk = 0;
+int set_rankk_chunk(int c) {
+  g_rankk_chunk = c;
+  return 0;
+}
+static int rankk_chunk(int m, int strips, int tiles, int mt, int kmax, int cmax, int sms) {
+  if (g_rankk_chunk > 0) return std::min(g_rankk_chunk, cmax);
+  const unsigned long long key = ((unsigned long long)m << 40) ^ ((unsigned long long)strips << 20) ^
+                                 ((unsigned long long)kmax << 8) ^ (unsigned long long)sms;
+  thread_local std::unordered_map<unsigned long long, int> cache;
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  const double s = (double)kmax / (8.0 * mt);
+  const double last = (double)(m - (tiles - 1) * mt) / mt;  // rows of the short last tile, in tiles
+  std::vector<double> load;
+  double cost[8] = {0};
+  double best = 1e300;
+  int ci = 0;
+  for (int c = cmax; c >= 1; c >>= 1, ++ci) {
+    const int chunks = (tiles + c - 1) / c;
+    const long long units = (long long)strips * chunks;
+    const int grid = (int)std::max(1LL, std::min(units, (long long)sms));
+    load.assign(grid, 0.0);
+    for (long long u = 0; u < units; ++u) {
+      const int ch = (int)(u % chunks);
+      const int nt = std::min(c, tiles - ch * c);
+      const bool has_last = ch == chunks - 1;
+      load[u % grid] += (has_last ? nt - 1 + last : nt) + s;
+    }
+    cost[ci] = *std::max_element(load.begin(), load.end());
+    best = std::min(best, cost[ci]);
+  }
+  int pick = 1;
+  ci = 0;
+  for (int c = cmax; c >= 1; c >>= 1, ++ci)
+    if (cost[ci] <= 1.02 * best) {
+      pick = c;
+      break;
+    }
+  cache.emplace(key, pick);
+  return pick;
+}
+
 template <bool TB, int KMAX, int MT, int WARPS_M, bool VEC>
 static int launch_rankk_v(cudaStream_t st, const GemmDesc& d, int sms) {
   using Cfg = RankkCfg<TB, KMAX, MT, WARPS_M>;
@@ -468,9 +527,10 @@ static int launch_rankk_v(cudaStream_t st, const GemmDesc& d, int sms) {
   }
   const int strips = (d.n + 63) / 64;
   const int tiles = (d.m + MT - 1) / MT;
-  const int units = strips * ((tiles + Cfg::CHUNK - 1) / Cfg::CHUNK);
+  const int chunk = rankk_chunk(d.m, strips, tiles, MT, KMAX, Cfg::CHUNK, sms);
+  const int units = strips * ((tiles + chunk - 1) / chunk);
   const int grid = std::max(1, std::min(units, sms));
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(d);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(d, chunk);
   note_launch();
   DC_CUDA_TRY(cudaGetLastError());
   return 0;
