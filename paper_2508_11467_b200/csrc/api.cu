@@ -24,6 +24,7 @@ extern double g_labrd_l2keep_min;
 extern int g_gebd2_cluster;
 int set_rankk_prefetch(int on);
 int set_rankk_chunk(int c);
+int set_rankk_bulk(int on);
 extern bool g_labrd_last_two_phase;
 extern int g_gemm_route;
 thread_local dcsvd_ctx* t_cur = nullptr;
@@ -367,6 +368,9 @@ int dcsvd_debug_rankk_prefetch(int on) { return dc::set_rankk_prefetch(on); }
 
 /* row tiles per work unit of the streaming rank-k kernel (0 = automatic; debug / tuning) */
 int dcsvd_debug_rankk_chunk(int c) { return dc::set_rankk_chunk(c); }
+
+/* A tiles of the streaming rank-k kernel by TMA bulk copies (1, default) or cp.async (0); debug */
+int dcsvd_debug_rankk_bulk(int on) { return dc::set_rankk_bulk(on); }
 
 /* L2 bytes of each large-panel GEMV pass loaded evict_last (0 = plain loads; debug / tuning) */
 int dcsvd_debug_labrd_l2keep(double bytes) {

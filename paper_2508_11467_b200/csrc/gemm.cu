@@ -23,8 +23,31 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 __constant__ int g_rankk_prefetch = 1;
+__constant__ int g_bulk_a = 1;  // rank-k A tiles by TMA bulk copies (debug: 0 = cp.async)
+int set_rankk_bulk(int on) { return cudaMemcpyToSymbol(g_bulk_a, &on, sizeof(int)) == cudaSuccess ? 0 : -1; }
 int set_rankk_prefetch(int on) {  // debug: L2 prefetch of the next C tile in the rank-k kernel
   return cudaMemcpyToSymbol(g_rankk_prefetch, &on, sizeof(int)) == cudaSuccess ? 0 : -1;
+}
+// TMA bulk copies (cp.async.bulk, async proxy) completing on an mbarrier.
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(a), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst), b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(d), "l"(src), "r"(bytes), "r"(b) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
@@ -310,8 +333,13 @@ static int launch_sized(cudaStream_t st, const GemmBatch* b, const GemmDesc* dd,
 // (<= 128): the GEBRD trailing update A -= P Q^T (bidiag.py:195-197) and the
 // CWY updates C -= Y X (qrblock.py:103-119).  Each CTA owns 64-column strips
 // of C: the K x 64 slice of op(B) is loaded once per strip and stays in shared
-// memory while MT-row tiles of A stream through a double-buffered cp.async
-// pipeline.  Each thread loads its C fragment into registers at the start of
+// memory while MT-row tiles of A stream through a double buffer: one TMA bulk
+// copy (cp.async.bulk, SASS UBLKCP) per tile column, issued by K threads spread
+// over the 8 warps and completing on the buffer's mbarrier (K arrivals + tx
+// bytes); tiles with an odd row count fall back to 16-byte cp.async pairs.
+// Bulk A copies: 8160^2 K=64 20.4 -> 21.6 TFLOP/s, 8192^2 K=128 22.3 -> 23.8
+// (tools/rankk_bulk_ab.py); issuing all of them from one warp was 25 % slower
+// than cp.async.  Each thread loads its C fragment into registers at the start of
 // a tile, so the HBM latency of the read-modify-write is covered by that
 // tile's DMMAs.  Persistent grid, 1 CTA / SM, 8 warps.
 template <bool TB, int KMAX, int MT, int WARPS_M>
@@ -351,7 +379,37 @@ __global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P, int ch
   const int chunks = (tiles + chunk - 1) / chunk;
   const int units = strips * chunks;
 
+  // A tiles by TMA bulk copies (one per column of the tile, issued by warp 0,
+  // completing on the buffer's mbarrier) when the rows allow 16-byte sizes;
+  // otherwise per-thread cp.async pairs.  g_gemm_route 7 (debug): cp.async only.
+  __shared__ __align__(8) uint64_t abar[2];
+  unsigned aphase = 0;  // bit b: parity of buffer b's next mbarrier phase
+  if (tid == 0) {
+    mbar_init(&abar[0], K);
+    mbar_init(&abar[1], K);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (Kp > K)  // pad columns K..Kp-1 of both A buffers are never copied: zero them once
+    for (int p = tid; p < 2 * (Kp - K) * MT; p += THREADS) {
+      const int b = p / ((Kp - K) * MT), r = p % ((Kp - K) * MT);
+      As[b * Cfg::A_ELEMS + (K + r / MT) * Cfg::LDA_S + r % MT] = 0.0;
+    }
+  __syncthreads();
+  auto bulk_ok = [&](int m0) { return VEC && g_bulk_a && ((min(MT, M - m0) & 1) == 0); };
+  auto load_a_bulk = [&](int buf, int m0) {  // thread kk < K copies column kk (K arrivals per phase)
+    const int rows = min(MT, M - m0);
+    const unsigned bytes = (unsigned)rows * 8u;
+    const int kk = (tid & 7) * 32 + (tid >> 3);  // spread the issuing threads over the 8 warps
+    if (kk < K) {
+      mbar_expect_tx(&abar[buf], bytes);
+      bulk_g2s(As + buf * Cfg::A_ELEMS + kk * Cfg::LDA_S, A + (long long)m0 + (long long)kk * lda, bytes, &abar[buf]);
+    }
+  };
   auto load_a = [&](int buf, int m0) {
+    if (bulk_ok(m0)) {
+      load_a_bulk(buf, m0);
+      return;
+    }
     double* as = As + buf * Cfg::A_ELEMS;
 #pragma unroll
     for (int p0 = 0; p0 < MT * KMAX / 2; p0 += THREADS) {  // A: [k][m], pairs along m (compile-time trip count)
@@ -422,6 +480,10 @@ __global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P, int ch
       }
       cp_async_commit();
       cp_async_wait<1>();
+      if (bulk_ok(m0)) {
+        mbar_wait(&abar[buf], (aphase >> buf) & 1u);
+        aphase ^= 1u << buf;
+      }
       __syncthreads();
       const double* as = As + buf * Cfg::A_ELEMS;
       double acc[Cfg::FM][Cfg::FN][2];
