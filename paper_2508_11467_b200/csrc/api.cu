@@ -25,6 +25,7 @@ extern int g_gebd2_cluster;
 int set_rankk_prefetch(int on);
 int set_rankk_chunk(int c);
 int set_rankk_bulk(int on);
+int set_rankk_min(long long mn);
 extern bool g_labrd_last_two_phase;
 extern int g_gemm_route;
 thread_local dcsvd_ctx* t_cur = nullptr;
@@ -371,6 +372,9 @@ int dcsvd_debug_rankk_chunk(int c) { return dc::set_rankk_chunk(c); }
 
 /* A tiles of the streaming rank-k kernel by TMA bulk copies (1, default) or cp.async (0); debug */
 int dcsvd_debug_rankk_bulk(int on) { return dc::set_rankk_bulk(on); }
+
+/* smallest C size (m*n) routed to the streaming rank-k kernel (<= 0: default 512^2); debug */
+int dcsvd_debug_rankk_min(long long mn) { return dc::set_rankk_min(mn); }
 
 /* L2 bytes of each large-panel GEMV pass loaded evict_last (0 = plain loads; debug / tuning) */
 int dcsvd_debug_labrd_l2keep(double bytes) {

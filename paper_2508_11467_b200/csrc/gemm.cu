@@ -536,6 +536,13 @@ __global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P, int ch
 // trailing matrices keep 8-tile units, small ones get short units that fill
 // the 148 SMs).  g_rankk_chunk > 0 forces it (debug).
 static int g_rankk_chunk = 0;
+// Smallest C (m*n) routed to the streaming kernel: 512^2 (tools/rankk_min_ab.py: ORMBR of 1024^2
+// 0.99 -> 0.95 ms; 256^2 no better).
+static long long g_rankk_min_mn = 512LL * 512;
+int set_rankk_min(long long mn) {
+  g_rankk_min_mn = mn > 0 ? mn : 512LL * 512;
+  return 0;
+}
 int set_rankk_chunk(int c) {
   g_rankk_chunk = c;
   return 0;
@@ -617,12 +624,12 @@ static int sm_count() {
   return g_sms;
 }
 
-// Route rank-k updates (K <= 128, large M x N, plain strided operands) to the
+// Route rank-k updates (K <= 128, M x N >= 512^2, plain strided operands) to the
 // streaming kernel.  Returns -1 when the shape does not qualify.
 static int try_rankk(cudaStream_t st, bool ta, bool tb, const GemmDesc& d) {
   if (g_gemm_route != 0) return -1;
   if (ta || d.acol || d.ccol || d.k < 1 || d.k > 128 || d.beta == 0.0) return -1;
-  if ((long long)d.m * d.n < (long long)1024 * 1024 || d.m < 256) return -1;
+  if ((long long)d.m * d.n < g_rankk_min_mn || d.m < 256) return -1;
   const int sms = sm_count();
   if (d.k <= 64) return tb ? launch_rankk<true, 64, 128, 4>(st, d, sms) : launch_rankk<false, 64, 128, 4>(st, d, sms);
   return tb ? launch_rankk<true, 128, 64, 2>(st, d, sms) : launch_rankk<false, 128, 64, 2>(st, d, sms);
