@@ -418,12 +418,14 @@ def test_c2_scale_square_8192(cuda):
 
 @pytest.mark.parametrize("k", [1, 37, 64, 100, 128])
 @pytest.mark.parametrize("tb", [False, True])
-def test_rank_k_update_kernel(cuda, k, tb):
+@pytest.mark.parametrize("m", [2000, 2001])
+def test_rank_k_update_kernel(cuda, k, tb, m):
     """Large rank-k updates take the streaming kernel (gemm.cu); compare with
-    a plain torch fp64 product."""
+    a plain torch fp64 product.  m = 2001 leaves an odd-row last tile, which
+    takes the cp.async fallback next to the TMA bulk-copied tiles."""
     g = _g()
     torch.manual_seed(k)
-    m, n = 2000, 1500
+    n = 1500
     a = torch.randn(m, k, dtype=torch.float64, device=cuda)
     b = torch.randn(n, k, dtype=torch.float64, device=cuda) if tb else torch.randn(k, n, dtype=torch.float64, device=cuda)
     c = torch.randn(n, m, dtype=torch.float64, device=cuda).t()  # column-major m x n
@@ -938,3 +940,37 @@ def test_wide_options_and_partial_sequences(cuda):
         ref[i:] -= fact.tauq[i] * np.outer(v, v @ ref[i:])
     out = g.ormqr_like(seq, c.copy(order="F"))
     np.testing.assert_allclose(out, ref, rtol=0, atol=1e-13)
+
+
+@pytest.mark.parametrize("k,tb", [(64, True), (128, False), (37, True)])
+def test_rank_k_bulk_matches_cp_async(cuda, k, tb):
+    """The streaming kernel's A tiles by TMA bulk copies and by per-thread
+    cp.async hold the same bytes, so C is bitwise identical; an A view at an
+    odd element offset (not 16-byte aligned) takes the 8-byte cp.async path."""
+    g = _g()
+    from paper_2508_11467_b200 import _lib
+    lib = _lib.load_library()
+    torch.manual_seed(3)
+    m, n = 3001, 2999
+    a = torch.randn(k, m, dtype=torch.float64, device=cuda).t()
+    b = (torch.randn(k, n, dtype=torch.float64, device=cuda).t() if tb
+         else torch.randn(n, k, dtype=torch.float64, device=cuda).t())
+    c0 = torch.randn(n, m, dtype=torch.float64, device=cuda).t()
+    out = []
+    try:
+        for bulk in (1, 0):
+            lib.dcsvd_debug_rankk_bulk(bulk)
+            c = c0.clone()
+            g.matmul_accumulate(-1.0, a, False, b, tb, 1.0, c)
+            out.append(c)
+    finally:
+        lib.dcsvd_debug_rankk_bulk(1)
+    assert torch.equal(out[0], out[1])
+    ref = c0 - a @ (b.t() if tb else b)
+    assert (out[0] - ref).abs().max().item() <= 1e-12 * k
+    store = torch.randn(k * (m + 1) + 1, dtype=torch.float64, device=cuda)
+    a_odd = store[1:1 + k * (m + 1)].view(k, m + 1).t()[:m]  # base at an odd element, ld = m + 1
+    a_odd.copy_(a)
+    c = c0.clone()
+    g.matmul_accumulate(-1.0, a_odd, False, b, tb, 1.0, c)
+    assert (c - ref).abs().max().item() <= 1e-12 * k
