@@ -37,6 +37,10 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
   unsigned a = (unsigned)__cvta_generic_to_shared(bar);
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(a) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
   unsigned a = (unsigned)__cvta_generic_to_shared(bar);
   asm volatile(
@@ -339,7 +343,7 @@ static int launch_sized(cudaStream_t st, const GemmBatch* b, const GemmDesc* dd,
 // bytes); tiles with an odd row count fall back to 16-byte cp.async pairs.
 // Bulk A copies: 8160^2 K=64 20.4 -> 21.6 TFLOP/s, 8192^2 K=128 22.3 -> 23.8
 // (tools/rankk_bulk_ab.py); issuing all of them from one warp was 25 % slower
-// than cp.async.  Each thread loads its C fragment into registers at the start of
+// than cp.async.  Bulk B strips on top: K=128 23.8 -> 24.1 (ORMBR 91.2 -> 90.0 ms).  Each thread loads its C fragment into registers at the start of
 // a tile, so the HBM latency of the read-modify-write is covered by that
 // tile's DMMAs.  Persistent grid, 1 CTA / SM, 8 warps.
 template <bool TB, int KMAX, int MT, int WARPS_M>
@@ -381,14 +385,22 @@ __global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P, int ch
 
   // A tiles by TMA bulk copies (one per column of the tile, issued by warp 0,
   // completing on the buffer's mbarrier) when the rows allow 16-byte sizes;
-  // otherwise per-thread cp.async pairs.  g_gemm_route 7 (debug): cp.async only.
-  __shared__ __align__(8) uint64_t abar[2];
-  unsigned aphase = 0;  // bit b: parity of buffer b's next mbarrier phase
+  // otherwise per-thread cp.async pairs (dcsvd_debug_rankk_bulk(0): cp.async only).
+  // The B strip of a unit likewise: one bulk copy per row (TB, K arrivals) or
+  // per column (K even, 64 arrivals) on abar[2].
+  __shared__ __align__(8) uint64_t abar[3];
+  unsigned aphase = 0;  // bit b: parity of barrier b's next phase
   if (tid == 0) {
     mbar_init(&abar[0], K);
     mbar_init(&abar[1], K);
+    mbar_init(&abar[2], TB ? K : NW);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  if (Kp > K)  // pad rows/columns K..Kp-1 of the B strip: zero once (bulk copies never write them)
+    for (int p = tid; p < (Kp - K) * NW; p += THREADS) {
+      const int kk = K + p / NW, j = p % NW;
+      Bs[TB ? kk * Cfg::LDB_S + j : j * Cfg::LDB_S + kk] = 0.0;
+    }
   if (Kp > K)  // pad columns K..Kp-1 of both A buffers are never copied: zero them once
     for (int p = tid; p < 2 * (Kp - K) * MT; p += THREADS) {
       const int b = p / ((Kp - K) * MT), r = p % ((Kp - K) * MT);
@@ -427,7 +439,24 @@ __global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P, int ch
     const int s = u / chunks, ch = u % chunks;
     const int n0 = s * NW;
     const int t0 = ch * chunk, t1 = min(tiles, t0 + chunk);
-    if (TB) {
+    const bool bbulk = VEC && g_bulk_a && (TB ? ((min(NW, N - n0) & 1) == 0) : ((K & 1) == 0));
+    if (bbulk) {
+      const int q = (tid & 7) * 32 + (tid >> 3);  // issuing threads spread over the warps
+      if (TB) {  // row kk of the strip: min(64, N - n0) contiguous doubles
+        if (q < K) {
+          const unsigned bytes = (unsigned)min(NW, N - n0) * 8u;
+          mbar_expect_tx(&abar[2], bytes);
+          bulk_g2s(Bs + q * Cfg::LDB_S, B + (long long)n0 + (long long)q * ldb, bytes, &abar[2]);
+        }
+      } else if (q < NW) {  // column j of the strip: K contiguous doubles
+        if (n0 + q < N) {
+          mbar_expect_tx(&abar[2], (unsigned)K * 8u);
+          bulk_g2s(Bs + q * Cfg::LDB_S, B + (long long)(n0 + q) * ldb, (unsigned)K * 8u, &abar[2]);
+        } else {
+          mbar_arrive(&abar[2]);
+        }
+      }
+    } else if (TB) {
       for (int p = tid; p < Kp * NW / 2; p += THREADS) {  // B[n + k*ldb]: pairs along n
         const int j = 2 * (p % (NW / 2)), kk = p / (NW / 2);
         const int gn = n0 + j;
@@ -483,6 +512,10 @@ __global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P, int ch
       if (bulk_ok(m0)) {
         mbar_wait(&abar[buf], (aphase >> buf) & 1u);
         aphase ^= 1u << buf;
+      }
+      if (t == t0 && bbulk) {
+        mbar_wait(&abar[2], (aphase >> 2) & 1u);
+        aphase ^= 4u;
       }
       __syncthreads();
       const double* as = As + buf * Cfg::A_ELEMS;
