@@ -55,14 +55,6 @@ def workload_flops(m, n):
     return flops_square(k)
 
 
-def philox_uniform(m, n, seed):
-    """MatrixSpec('random', m, n, seed) input (harness.py:69-78, 139-142),
-    column-major, generated with numpy's Philox on the host."""
-    w = np.random.Philox(key=seed).random_raw(m * n)
-    u = ((w >> np.uint64(11)).astype(np.float64) + 0.5) * 2.0 ** -53
-    return u.reshape((n, m))  # row j of this array = column j of A (column-major)
-
-
 class ClockSampler:
     """Samples SM clock and throttle reasons via NVML during the timed region."""
 
@@ -135,22 +127,52 @@ def load_ncu_traffic():
     return None
 
 
-def cpu_sample(n, threads, seed=1):
-    """Time the oracle (reference algorithm port) on an n x n random matrix in
-    a subprocess with `threads` BLAS threads; returns seconds."""
-    code = (
-        "import sys,time,numpy as np; sys.path.insert(0, %r); import oracle;"
-        "a=oracle.make_matrix('random',%d,%d,seed=%d); t=time.perf_counter(); oracle.svd(a);"
-        "print(time.perf_counter()-t)" % (ROOT, n, n, seed)
-    )
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def ref_kind():
+    """"reference" when the unmodified reference package is installed in
+    baseline/_ref (pip --target), else the oracle
+    port ("port")."""
+    return "reference" if os.path.isfile(os.path.join(REF_DIR, "dcsvd", "driver.py")) else "port"
+
+
+def cpu_sample(n, threads, seed=1, m=None, values_only=False):
+    """Time one CPU SVD (the real reference's `dcsvd.gesdd` from baseline/_ref
+    when installed, else the oracle port) of MatrixSpec('random', m, n, seed)
+    in a subprocess with `threads` BLAS threads; returns seconds."""
+    m = n if m is None else m
+    if ref_kind() == "reference":
+        code = (
+            "import sys,time; sys.path.insert(0, %r); import dcsvd;"
+            "a=dcsvd.generate_matrix(dcsvd.MatrixSpec('random',%d,%d,seed=%d)); t=time.perf_counter();"
+            "dcsvd.gesdd(a, dcsvd.SVDOptions(want_vectors=%r)); print(time.perf_counter()-t)"
+            % (REF_DIR, m, n, seed, not values_only)
+        )
+    else:
+        code = (
+            "import sys,time,numpy as np; sys.path.insert(0, %r); import oracle;"
+            "a=oracle.make_matrix('random',%d,%d,seed=%d); t=time.perf_counter(); oracle.svd(a);"
+            "print(time.perf_counter()-t)" % (ROOT, m, n, seed)
+        )
     env = dict(os.environ)
     for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
         env[k] = str(threads)
     env["PYTHONDONTWRITEBYTECODE"] = "1"
-    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=900)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=3600)
     if out.returncode != 0:
         raise RuntimeError(out.stderr)
     return float(out.stdout.strip().splitlines()[-1])
+
+
+def cpu_parallel(n, procs, seed0):
+    """`procs` concurrent single-thread CPU SVDs of n x n (seeds seed0..):
+    the SURVEY 8(d) C5 plan (one BLAS thread per process, one process per
+    core).  Returns the wall seconds of the slowest."""
+    import concurrent.futures as cf
+    with cf.ThreadPoolExecutor(max_workers=procs) as ex:
+        ts = list(ex.map(lambda i: cpu_sample(n, 1, seed=seed0 + i), range(procs)))
+    return max(ts)
 
 
 def host_cores():
@@ -167,28 +189,154 @@ def dist_env():
     return ws, rank, local
 
 
+def free_port():
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
+def maybe_spawn(args):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-launch this
+    script under torch.distributed.run with N ranks (one process per GPU,
+    rendezvous on 127.0.0.1) and return its exit code."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    print("[bench] spawning %d ranks: %s" % (args.gpus, " ".join(cmd)), file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def init_dist(torch, dist, ws, rank, local):
+    """One process per GPU; NCCL process group when ws > 1 (logged).  More
+    ranks than GPUs (a world-size-2 check on a 1-GPU box) share GPUs
+    round-robin over a gloo group: NCCL refuses two ranks on one device."""
+    ndev = torch.cuda.device_count()
+    dev = local % max(ndev, 1)
+    torch.cuda.set_device(dev)
+    if ws > 1:
+        if ws <= ndev:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+            nccl = ".".join(map(str, torch.cuda.nccl.version()))
+            print(f"[bench] rank {rank}/{ws}: NCCL {nccl} process group initialised on cuda:{dev}",
+                  file=sys.stderr, flush=True)
+        else:
+            dist.init_process_group("gloo")
+            print(f"[bench] rank {rank}/{ws}: {ws} ranks > {ndev} GPU(s): gloo process group, ranks share "
+                  f"cuda:{dev}", file=sys.stderr, flush=True)
+    return dev
+
+
+def max_over_ranks(torch, dist, ws, local, v):
+    if ws <= 1:
+        return v
+    on_gpu = dist.get_backend() == "nccl"
+    t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}" if on_gpu else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def load_sigma_fixture(tag):
+    """Reference sigma on the same Philox input bytes (tests/golden/make_large_sigma.py)."""
+    p = os.path.join(ROOT, "tests", "golden", f"{tag}_sigma.npz")
+    if not os.path.exists(p):
+        return None
+    return np.load(p)
+
+
+def sigma_rel(sig, ref):
+    """max_i |sigma_i - sigma_i^ref| / sigma_max (north-star check, tolerance 1e-12 n)."""
+    sig = np.asarray(sig, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    return float(np.max(np.abs(sig - ref)) / ref[0])
+
+
 def run_reference(args):
+    """--impl reference: the reference's own CPU implementation (the unmodified
+    `dcsvd` package in baseline/_ref when installed, else the oracle port) on
+    this host's cores, on a bounded sample of the workload per step."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
     m, n, seed, desc = WORKLOADS[args.workload]
     cores = host_cores()
-    # bounded sample: square n_s chosen so (K + W) steps take ~2-3 minutes
-    n_s = int(min(n, 2048 * (150.0 / (21.0 * max(args.steps, 1))) ** (1.0 / 3.0)) // 128 * 128)
-    n_s = max(n_s, 256)
-    for _ in range(args.warmup):
-        cpu_sample(256, cores)
-    times = [cpu_sample(n_s, cores) for _ in range(args.steps)]
-    t = float(np.mean(times))
-    val = flops_square(n_s) / t / 1e9
-    sample = f"oracle port (numpy, {cores} BLAS threads) full SVD of a {n_s}x{n_s} random matrix per step; C2 itself takes ~711 s on 8 threads (BASELINE.md)"
+    kind = ref_kind()
+    who = "reference dcsvd 0.1.0 (baseline/_ref)" if kind == "reference" else "oracle port (numpy restatement)"
+    steps = max(args.steps, 1)
+    if args.workload == "c5":
+        # full-size C5 items, one single-thread process per core (SURVEY 8d)
+        procs = max(1, min(cores, 64))
+        for _ in range(args.warmup):
+            cpu_sample(128, 1)
+        times = [cpu_parallel(n, procs, 1000 + 1000 * s_) for s_ in range(steps)]
+        t = float(np.mean(times))
+        svd_s = procs / t
+        val, unit = svd_s, "SVD/s"
+        metric = "batched fp64 SVD (U,S,V) throughput, 2048x2048 items"
+        sample = (f"{who}: {procs} concurrent processes x 1 BLAS thread, one full 2048^2 SVD each per step "
+                  f"(seeds 1000+i); 512 items extrapolate to {512 / svd_s:.0f} s")
+        cfg = {"workload": desc, "m": m, "n": n, "items_per_step": procs}
+        ms = t * 1e3
+        hib = True
+    elif args.workload == "c4":
+        # BDC only on the C4 fixture (n = 16384) takes ~57 s with vectors: time
+        # the reference bdsdc on a leading n_s slice of the same bidiagonal
+        n_s = 4096
+        fx = os.path.join(ROOT, "tests", "golden", "c4_n16384.npz")
+        if kind == "reference":
+            code = ("import sys,time,numpy as np; sys.path.insert(0,%r); import dcsvd;"
+                    "z=np.load(%r); p=dcsvd.BidiagonalProblem(z['d'][:%d].copy(), z['e'][:%d].copy());"
+                    "t=time.perf_counter(); dcsvd.bdsdc(p); print(time.perf_counter()-t)"
+                    % (REF_DIR, fx, n_s, n_s - 1))
+        else:
+            code = ("import sys,time,numpy as np; sys.path.insert(0,%r); import oracle;"
+                    "z=np.load(%r); p=oracle.Bidiag(z['d'][:%d].copy(), z['e'][:%d].copy());"
+                    "t=time.perf_counter(); oracle.bdc(p); print(time.perf_counter()-t)"
+                    % (ROOT, fx, n_s, n_s - 1))
+        env = dict(os.environ, OPENBLAS_NUM_THREADS=str(cores), PYTHONDONTWRITEBYTECODE="1")
+        times = []
+        for i in range(args.warmup + steps):
+            out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=3600)
+            if out.returncode != 0:
+                raise RuntimeError(out.stderr)
+            if i >= args.warmup:
+                times.append(float(out.stdout.strip().splitlines()[-1]))
+        t = float(np.mean(times))
+        val, unit, ms, hib = t, "s", t * 1e3, False
+        metric = "BDC stage time (bdsdc with vectors), seconds"
+        sample = (f"{who} bdsdc with vectors on the leading {n_s} x {n_s} block of the C4 fixture bidiagonal, "
+                  f"{cores} BLAS threads; the full n=16384 fixture takes 57.2 s with vectors (BASELINE.md)")
+        cfg = {"workload": desc, "n": n, "sample_n": n_s}
+    else:
+        # bounded sample with the workload's shape: square n_s (C1/C2) or a
+        # 64:1 tall-skinny m_s x n_s (C3) sized so K + W steps take minutes
+        if args.workload == "c3":
+            n_s, m_s = 256, 256 * 64
+        else:
+            n_s = int(min(n, 2048 * (150.0 / (21.0 * steps)) ** (1.0 / 3.0)) // 128 * 128)
+            n_s = max(n_s, 256)
+            m_s = n_s
+        for _ in range(args.warmup):
+            cpu_sample(256, cores)
+        times = [cpu_sample(n_s, cores, m=m_s) for _ in range(steps)]
+        t = float(np.mean(times))
+        val, unit, ms, hib = workload_flops(m_s, n_s) / t / 1e9, "GFLOP/s", t * 1e3, True
+        metric = "fp64 SVD (U,S,V) GFLOP/s (28/3 n^3 convention)"
+        sample = (f"{who}, {cores} BLAS threads, full SVD of MatrixSpec('random',{m_s},{n_s}) per step; "
+                  "C2 itself took 711.5 s on 8 survey-host threads (BASELINE.md)")
+        cfg = {"workload": desc, "m": m, "n": n, "sample_m": m_s, "sample_n": n_s}
     line = {
-        "impl": "reference", "metric": "fp64 SVD (U,S,V) GFLOP/s (28/3 n^3 convention)", "value": val,
-        "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": desc, "m": m, "n": n, "sample_n": n_s},
-        "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": cores, "kind": "port", "sample": sample},
-        "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": metric, "value": val,
+        "unit": unit, "n_gpus": ws, "steps": steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": hib, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": cfg,
+        "cpu_baseline": {"value": val, "unit": unit, "cores": cores if args.workload != "c5" else cfg["items_per_step"],
+                         "kind": kind, "sample": sample},
+        "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -289,9 +437,12 @@ def run_c4(args, dcs, _lib, torch, dist, ws, rank, local):
     torch.cuda.synchronize()
     t_vo = time.perf_counter() - t0
     line = {
-        "metric": "BDC (bdsdc with vectors) GFLOP/s, nominal 8/3 n^3", "value": F / (t_ms * 1e-3) / 1e9,
-        "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "metric": "BDC stage time (bdsdc with vectors), seconds", "value": t_ms * 1e-3,
+        "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "executed_merge_gemm_flops": g_flops / max(args.steps, 1),
+        "note": "heavy deflation: the nominal 8/3 n^3 = %.3g flop is not executed; the merge GEMMs run the "
+                "executed_merge_gemm_flops count" % F,
         "data": "C4 fixture tests/golden/c4_n16384.npz (LAPACK dgebrd of U diag(sigma) V^T, 8 clusters)",
         "config": {"workload": WORKLOADS["c4"][3], "n": n},
         "accuracy": {"max_abs_sigma_vs_reference": float(np.max(np.abs(vals - z["sigma_ref"]))),
@@ -303,12 +454,31 @@ def run_c4(args, dcs, _lib, torch, dist, ws, rank, local):
         "roofline": roof_c4[0],
         "roofline_secondary": roof_c4[1],
         "clocks": clk.summary(),
-        "e2e": {"value": F / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
+        "e2e": {"value": e2e_ms * 1e-3, "unit": "s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
-        "cpu_baseline": {"value": float(F / float(z["ref_seconds_values_only"]) / 1e9), "unit": "GFLOP/s", "cores": 7,
-                         "kind": "reference", "seconds": float(z["ref_seconds_values_only"]),
-                         "sample": "reference dcsvd.bdsdc values-only on the same fixture, build container (7 BLAS threads), timed when the fixture was made; with vectors it took 57.2 s (BASELINE.md)"},
+        "reference_full_size": {"seconds_with_vectors": 57.2, "seconds_values_only": float(z["ref_seconds_values_only"]),
+                                "where": "build container, 7 BLAS threads (BASELINE.md §2; fixture creation)"},
     }
+    if not args.no_cpu_baseline and ws == 1:
+        n_s, cores = 4096, host_cores()
+        kind = ref_kind()
+        fx = os.path.join(ROOT, "tests", "golden", "c4_n16384.npz")
+        if kind == "reference":
+            code = ("import sys,time,numpy as np; sys.path.insert(0,%r); import dcsvd;"
+                    "z=np.load(%r); p=dcsvd.BidiagonalProblem(z['d'][:%d].copy(), z['e'][:%d].copy());"
+                    "t=time.perf_counter(); dcsvd.bdsdc(p); print(time.perf_counter()-t)" % (REF_DIR, fx, n_s, n_s - 1))
+        else:
+            code = ("import sys,time,numpy as np; sys.path.insert(0,%r); import oracle;"
+                    "z=np.load(%r); p=oracle.Bidiag(z['d'][:%d].copy(), z['e'][:%d].copy());"
+                    "t=time.perf_counter(); oracle.bdc(p); print(time.perf_counter()-t)" % (ROOT, fx, n_s, n_s - 1))
+        env = dict(os.environ, OPENBLAS_NUM_THREADS=str(cores), PYTHONDONTWRITEBYTECODE="1")
+        out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=1800)
+        if out.returncode == 0:
+            t_cpu = float(out.stdout.strip().splitlines()[-1])
+            line["cpu_baseline"] = {"value": t_cpu, "unit": "s", "cores": cores, "kind": kind,
+                                    "sample": f"bdsdc with vectors on the leading {n_s}x{n_s} block of the C4 "
+                                              f"fixture bidiagonal ({kind}), {cores} BLAS threads; the full "
+                                              "n=16384 fixture: 57.2 s with vectors (reference_full_size)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
@@ -324,7 +494,11 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--batch", type=int, default=16, help="C5: matrices per GPU per step")
+    ap.add_argument("--c5-total", type=int, default=512, help="C5: matrices in the whole job (sharded over ranks)")
     args = ap.parse_args()
+    rc = maybe_spawn(args)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference(args)
 
@@ -332,9 +506,7 @@ def main():
     import torch.distributed as dist
 
     ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    local = init_dist(torch, dist, ws, rank, local)
     import paper_2508_11467_b200 as dcs
     from paper_2508_11467_b200 import _lib
 
@@ -342,17 +514,30 @@ def main():
     if args.workload == "c4":
         return run_c4(args, dcs, _lib, torch, dist, ws, rank, local)
     k = min(m, n)
-    batch = args.batch if args.workload == "c5" else 1
-    # inputs: rank-specific seeds for replicas / shards
-    host = []
-    for b in range(batch):
-        s = seed + rank * batch + b if args.workload == "c5" else seed
-        host.append(torch.from_numpy(philox_uniform(m, n, s)).pin_memory())  # (n, m) row-major == A col-major
-    dev_inputs = [h.to(f"cuda:{local}").t() for h in host]  # m x n column-major views
+    c5 = args.workload == "c5"
+    if c5:
+        # BASELINE config 5: c5_total independent SVDs, contiguous shards per
+        # rank (batch.shard_range), no data-path collective
+        from paper_2508_11467_b200.batch import gather_sigma, shard_range
+        lo, hi = shard_range(args.c5_total, ws, rank)
+        seeds = [seed + i for i in range(lo, hi)]
+    else:
+        lo, hi, seeds = 0, 1, [seed]  # single SVD: every rank runs a replica
+    batch = len(seeds)
+    # inputs: MatrixSpec('random', m, n, seed) bytes from the GPU Philox
+    # (bit-identical to harness._Stream), mirrored once into pinned host
+    # memory for the end-to-end pass
+    dev_inputs, host = [], []
+    for s_ in seeds:
+        a = dcs.generate_matrix(dcs.MatrixSpec("random", m, n, seed=s_), device=True)
+        dev_inputs.append(a)
+        h = torch.empty((n, m), dtype=torch.float64).pin_memory()  # (n, m) row-major == A col-major
+        h.copy_(a.t())
+        host.append(h)
     F = workload_flops(m, n) * batch
 
     def step():
-        if batch == 1:
+        if not c5:
             return dcs.gesdd(dev_inputs[0])
         return dcs.gesdd_batched(dev_inputs)
 
@@ -392,10 +577,7 @@ def main():
     lib.dcsvd_debug_batch_streams.restype = ctypes.c_int
     streams = max(1, lib.dcsvd_debug_batch_streams(_lib.handle()))
     _lib.set_stats(False)
-    if ws > 1:
-        tt = torch.tensor([t_ms], device=f"cuda:{local}")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = float(tt.item())
+    t_ms = max_over_ranks(torch, dist, ws, local, t_ms)
     value = F * ws / (t_ms * 1e-3) / 1e9
 
     # --- e2e through the public numpy-free API with pinned host buffers
@@ -411,7 +593,7 @@ def main():
         for hb in host:
             devs.append(hb.to(f"cuda:{local}", non_blocking=True).t())
             h2d += hb.numel() * 8
-        rs = [dcs.gesdd(devs[0])] if batch == 1 else dcs.gesdd_batched(devs)
+        rs = dcs.gesdd_batched(devs) if c5 else [dcs.gesdd(devs[0])]
         for r in rs:
             out_s.copy_(r.sigma, non_blocking=True)
             out_u.copy_(r.u.t(), non_blocking=True)
@@ -428,10 +610,7 @@ def main():
     e1.record(stream)
     barrier()
     e2e_ms = max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3) / args.e2e_steps
-    if ws > 1:
-        tt = torch.tensor([e2e_ms], device=f"cuda:{local}")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
+    e2e_ms = max_over_ranks(torch, dist, ws, local, e2e_ms)
     e2e_value = F * ws / (e2e_ms * 1e-3) / 1e9
 
     # --- accuracy of the last device result on this rank (north-star checks),
@@ -441,6 +620,22 @@ def main():
     resid = rep.e_svd / max(m, n)
     orth_u = rep.orth_u / k
     orth_v = rep.orth_v / k
+    fx = load_sigma_fixture(args.workload)
+    sig_items = 1
+    if c5:
+        # sigma of the whole sharded batch gathered to every rank (NCCL
+        # all-gather, off the timed path), compared with the reference on the
+        # fixture's seeds
+        rs = dcs.gesdd_batched(dev_inputs, dcs.SVDOptions(want_vectors=False))
+        full = gather_sigma(torch.stack([x.sigma for x in rs]), args.c5_total).cpu().numpy()
+        del rs
+        sig_rel, sig_items = None, 0
+        if fx is not None:
+            cnt = min(len(fx["sigma"]), args.c5_total)
+            sig_rel = max(sigma_rel(full[i], fx["sigma"][i]) for i in range(cnt))
+            sig_items = cnt
+    else:
+        sig_rel = sigma_rel(r.sigma.cpu().numpy(), fx["sigma"]) if fx is not None else None
     prof = dcs.phase_profile(dev_inputs[0])
 
     if rank != 0:
@@ -486,38 +681,65 @@ def main():
                 "instrumented pass of the same K steps after the timed pass)" + note_streams,
     }
     roof, roof2 = (roof_lab, roof_gem) if lab_ms >= gem_ms else (roof_gem, roof_lab)
+    if c5:
+        svd_s = args.c5_total / (t_ms * 1e-3)
+        metric, val, unit = f"batched fp64 SVD (U,S,V) throughput, {args.c5_total} x {m}x{n}", svd_s, "SVD/s"
+        e2e_val = args.c5_total / (e2e_ms * 1e-3)
+    else:
+        metric, val, unit = "fp64 SVD (U,S,V) GFLOP/s (28/3 n^3 convention)", value, "GFLOP/s"
+        e2e_val = e2e_value
     line = {
-        "metric": "fp64 SVD (U,S,V) GFLOP/s (28/3 n^3 convention)",
-        "value": value,
-        "unit": "GFLOP/s",
+        "metric": metric,
+        "value": val,
+        "unit": unit,
+        "gflops": value,
         "n_gpus": ws,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": t_ms,
-        "seconds_per_svd": t_ms * 1e-3 / batch,
+        "seconds_per_svd": t_ms * 1e-3 / (args.c5_total if c5 else 1),  # whole job (c5) / one replica
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if c5 else "weak",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (Philox MatrixSpec('random') inputs, BASELINE.md §3)",
         "config": {"workload": desc, "m": m, "n": n, "batch_per_gpu": batch,
-                   "parallelism": f"replicas x{ws}" if batch == 1 else f"batch shards x{ws}",
+                   **({"batch_total": args.c5_total, "shard_rank0": [lo, hi]} if c5 else {}),
+                   "parallelism": f"batch shards x{ws} ({dist.get_backend() if ws > 1 else 'single process'})"
+                   if c5 else f"replicas x{ws}",
                    "l2": "input 512 MiB > 126 MB L2 (no flush needed)" if m * n * 8 > 2 ** 28 else "input fits L2; timed back-to-back"},
         "phases_s": dict(prof.phases),
-        "accuracy": {"resid_scaled": resid, "orth_u_scaled": orth_u, "orth_v_scaled": orth_v},
+        "accuracy": {"sigma_rel_vs_reference": sig_rel, "sigma_tol": 1e-12 * k,
+                     "sigma_reference": (f"tests/golden/{args.workload}_sigma.npz: reference dcsvd.gesdd values-only on "
+                                         f"the same MatrixSpec('random',{m},{n},seed=...) bytes, {sig_items} item(s)")
+                     if fx is not None else None,
+                     "resid_scaled": resid, "orth_u_scaled": orth_u, "orth_v_scaled": orth_v, "tol": 1e-14,
+                     "pass": bool((sig_rel is None or sig_rel <= 1e-12 * k) and resid <= 1e-14 and orth_u <= 1e-14
+                                  and orth_v <= 1e-14)},
         "gpu_launches": int(launches),
         "roofline": roof,
         "roofline_secondary": roof2,
         "clocks": clk.summary(),
-        "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+        "e2e": {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_ms},
     }
-    if not args.no_cpu_baseline:
-        n_s = 1536
-        t_cpu = cpu_sample(n_s, 1)
-        line["cpu_baseline"] = {"value": flops_square(n_s) / t_cpu / 1e9, "unit": "GFLOP/s", "cores": 1,
-                                "kind": "port", "seconds": t_cpu,
-                                "sample": f"oracle port (numpy restatement of the reference), 1 BLAS thread, full SVD of MatrixSpec('random',{n_s},{n_s},seed=1)"}
+    if not args.no_cpu_baseline and ws == 1:
+        kind = ref_kind()
+        who = "reference dcsvd 0.1.0 (baseline/_ref)" if kind == "reference" else "oracle port (numpy restatement)"
+        if c5:
+            procs = max(1, min(host_cores(), 64))
+            t_cpu = cpu_parallel(n, procs, seed)
+            line["cpu_baseline"] = {"value": procs / t_cpu, "unit": "SVD/s", "cores": procs, "kind": kind,
+                                    "seconds": t_cpu,
+                                    "sample": f"{who}: {procs} concurrent single-thread processes, one full "
+                                              f"{m}x{n} SVD with vectors each (seeds {seed}..{seed + procs - 1})"}
+        else:
+            n_s = 1536 if kind == "reference" else 2048
+            t_cpu = cpu_sample(n_s, 1)
+            line["cpu_baseline"] = {"value": flops_square(n_s) / t_cpu / 1e9, "unit": "GFLOP/s", "cores": 1,
+                                    "kind": kind, "seconds": t_cpu,
+                                    "sample": f"{who}, 1 BLAS thread (the reference's own pin, conftest.py), full "
+                                              f"SVD with vectors of MatrixSpec('random',{n_s},{n_s},seed=1)"}
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()

@@ -6,6 +6,7 @@ point raises.  PyTorch provides device memory and the current stream.
 """
 
 import ctypes
+import functools
 import os
 import threading
 
@@ -153,6 +154,41 @@ def check(rc, h):
     if rc == ESINGULAR:
         raise np.linalg.LinAlgError(msg)
     raise RuntimeError(msg)
+
+
+def _cuda_devices(obj, out, depth=0):
+    if isinstance(obj, torch.Tensor):
+        if obj.is_cuda:
+            out.add(obj.device.index)
+    elif depth < 2 and isinstance(obj, (list, tuple)):
+        for x in obj:
+            _cuda_devices(x, out, depth + 1)
+    elif depth < 2 and isinstance(obj, dict):
+        for x in obj.values():
+            _cuda_devices(x, out, depth + 1)
+    elif depth < 1 and hasattr(obj, "__dict__") and not isinstance(obj, type):
+        for x in vars(obj).values():  # dataclass containers (problems, reflector sequences, results)
+            _cuda_devices(x, out, depth + 1)
+
+
+def on_input_device(fn):
+    """Run a public entry point on the device its CUDA tensor arguments live
+    on (handle, stream and outputs all follow ``torch.cuda.current_device``);
+    numpy-only calls use the current device.  Mixed devices are rejected."""
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        devs = set()
+        for x in list(args) + list(kwargs.values()):
+            _cuda_devices(x, devs)
+        if len(devs) > 1:
+            raise ValueError(f"arguments live on different CUDA devices {sorted(devs)}")
+        if not devs or not torch.cuda.is_available():
+            return fn(*args, **kwargs)
+        with torch.cuda.device(devs.pop()):
+            return fn(*args, **kwargs)
+
+    return wrapper
 
 
 def stream_ptr():

@@ -40,6 +40,35 @@ def gather_to_owner(local_items, dst=0, group=None):
     return full
 
 
+def gather_sigma(local_sigma, total, group=None):
+    """All-gather the singular values of a sharded batch: ``local_sigma`` is
+    this rank's (hi - lo) x k tensor for its ``shard_range`` slice; returns
+    the total x k tensor in global batch order on every rank.  NCCL
+    all-gather of device tensors (padded to the largest shard); with a gloo
+    group the payload goes through host memory.  One 16 KiB row per SVD, off
+    the timed path."""
+    if not dist.is_initialized():
+        return local_sigma
+    ws = dist.get_world_size(group)
+    k = int(local_sigma.shape[1]) if local_sigma.dim() == 2 else 0
+    cap = -(-total // ws)
+    on_gpu = dist.get_backend(group) == "nccl"
+    buf = torch.zeros((cap, k), dtype=torch.float64, device=local_sigma.device if on_gpu else "cpu")
+    buf[: local_sigma.shape[0]] = local_sigma.to(buf.device)
+    out = torch.empty((ws * cap, k), dtype=torch.float64, device=buf.device)
+    if on_gpu:
+        dist.all_gather_into_tensor(out, buf, group=group)
+    else:
+        parts = [torch.empty_like(buf) for _ in range(ws)]
+        dist.all_gather(parts, buf, group=group)
+        out = torch.cat(parts)
+    rows = []
+    for r in range(ws):
+        lo, hi = shard_range(total, ws, r)
+        rows.append(out[r * cap: r * cap + (hi - lo)])
+    return torch.cat(rows)
+
+
 def batched_svd_sharded(make_matrix, total, options=None, gather=False):
     """Solve matrices [0, total) across the process group: this rank builds
     its slice with ``make_matrix(i)`` (returns an m x n array/tensor) and runs

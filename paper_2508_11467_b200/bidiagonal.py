@@ -64,6 +64,7 @@ def _out_vec(t, like_np):
     return t.cpu().numpy() if like_np else t
 
 
+@_lib.on_input_device
 def gebrd_blocked(a, block=32):
     """Blocked one-stage bidiagonalization in place (bidiag.py:168-204):
     cooperative LABRD panel kernel + one DMMA trailing GEMM per panel."""
@@ -86,12 +87,14 @@ def gebrd_blocked(a, block=32):
                                    _out_vec(tp, was_np))
 
 
+@_lib.on_input_device
 def gebrd_unblocked(a):
     """Unblocked (GEBD2) reduction in place (bidiag.py:75-110)."""
     m, n = _require_tall(tuple(a.shape))
     return gebrd_blocked(a, block=max(n, 1))
 
 
+@_lib.on_input_device
 def labrd_panel(a, block, work, d, e, tauq, taup):
     """One merged rank-(2 block) panel of the view ``a`` (bidiag.py:113-165).
     Writes the panel rows/columns of ``a`` and the d/e/tauq/taup segments;

@@ -29,6 +29,7 @@ class GivensRotation:
     s: float
 
 
+@_lib.on_input_device
 def householder_generate(alpha, x):
     """Reflector mapping (alpha, x) onto (pivot, 0...), no safmin rescaling
     (densecore.py:114-128); one GPU kernel (norm, scalars, essential)."""
@@ -46,6 +47,7 @@ def householder_generate(alpha, x):
     return HouseholderReflector(tau, ess if torch_in else ess.cpu().numpy(), beta)
 
 
+@_lib.on_input_device
 def givens_generate(a, b):
     """(GivensRotation, r) with c a + s b = r >= 0 (densecore.py:131-140)."""
     h = _lib.handle()
@@ -63,6 +65,7 @@ def ctypes_offset(t, elems):
     return ctypes.c_void_p(t.data_ptr() + 8 * elems)
 
 
+@_lib.on_input_device
 def triangular_solve(t, b, side="left", trans=False):
     """Solve against an upper-triangular T in place on ``b``
     (densecore.py:143-171): left B <- T^-1 B (T^-T B), right B <- B T^-1 (B T^-T).
@@ -97,6 +100,7 @@ def _op_shape(shape, trans):
     return (shape[1], shape[0]) if trans else tuple(shape)
 
 
+@_lib.on_input_device
 def matmul_accumulate(alpha, a, trans_a, b, trans_b, beta, c):
     """C <- beta*C + alpha*op(A) op(B), in place into ``c`` (densecore.py:73-93);
     beta == 0 overwrites C without reading it.  DMMA kernel."""
@@ -122,6 +126,7 @@ def matmul_accumulate(alpha, a, trans_a, b, trans_b, beta, c):
     return c
 
 
+@_lib.on_input_device
 def matvec_accumulate(alpha, a, trans_a, x, beta, y):
     """y <- beta*y + alpha*op(A) x, in place (densecore.py:96-111)."""
     ma, ka = _op_shape(a.shape, trans_a)

@@ -30,6 +30,27 @@ extern bool g_labrd_last_two_phase;
 extern int g_gemm_route;
 thread_local dcsvd_ctx* t_cur = nullptr;
 
+int func_attr(const void* fn, int attr, int value) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, long long>, int>> done;  // ((fn, dev<<8|attr), value)
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return (int)e;
+  const long long key = ((long long)dev << 8) | attr;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& r : done)
+    if (r.first.first == fn && r.first.second == key && r.second == value) return 0;
+  e = cudaFuncSetAttribute(fn, (cudaFuncAttribute)attr, value);
+  if (e != cudaSuccess) return (int)e;
+  for (auto& r : done)
+    if (r.first.first == fn && r.first.second == key) {
+      r.second = value;
+      return 0;
+    }
+  done.push_back({{fn, key}, value});
+  return 0;
+}
+
 int set_error(dcsvd_ctx* h, int code, const char* fmt, ...) {
   char buf[512];
   va_list ap;
@@ -131,22 +152,28 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 __global__ void transpose_kernel(int rows, int cols, const double* __restrict__ A, long long lda, double* __restrict__ B,
                                  long long ldb) {
   // B (cols x rows) = A^T
+  // 32x32 tiles, grid-strided over both dimensions (any rows/cols < 2^31)
   __shared__ double tile[32][33];
-  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  for (int k = ty; k < 32; k += 8) {
-    const int r = bx + tx, c = by + k;
-    tile[k][tx] = (r < rows && c < cols) ? A[r + (long long)c * lda] : 0.0;
-  }
-  __syncthreads();
-  for (int k = ty; k < 32; k += 8) {
-    const int r = bx + k, c = by + tx;
-    if (r < rows && c < cols) B[c + (long long)r * ldb] = tile[tx][k];
+  const long long tr = (rows + 31) / 32, tc = (cols + 31) / 32;
+  for (long long t = blockIdx.x; t < tr * tc; t += gridDim.x) {
+    const int bx = (int)(t % tr) * 32, by = (int)(t / tr) * 32;
+    for (int k = ty; k < 32; k += 8) {
+      const int r = bx + tx, c = by + k;
+      tile[k][tx] = (r < rows && c < cols) ? A[r + (long long)c * lda] : 0.0;
+    }
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+      const int r = bx + k, c = by + tx;
+      if (r < rows && c < cols) B[c + (long long)r * ldb] = tile[tx][k];
+    }
+    __syncthreads();
   }
 }
 int transpose(cudaStream_t st, int rows, int cols, const double* A, long long lda, double* B, long long ldb) {
   if (rows <= 0 || cols <= 0) return 0;
-  transpose_kernel<<<dim3((rows + 31) / 32, (cols + 31) / 32), 256, 0, st>>>(rows, cols, A, lda, B, ldb);
+  const long long tiles = ((rows + 31LL) / 32) * ((cols + 31LL) / 32);
+  transpose_kernel<<<(unsigned)std::min<long long>(tiles, 148LL * 16), 256, 0, st>>>(rows, cols, A, lda, B, ldb);
   note_launch();
   DC_CUDA_TRY(cudaGetLastError());
   return 0;
@@ -252,7 +279,10 @@ int square_core(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double*
   DC_CUDA_TRY(cudaStreamWaitEvent(sd->own_stream, h->ev_fork, 0));
   rc = ormbr_run(sd, sd->own_stream, 'P', true, m, n, A, lda, tp, VT, n, n, ldvt, kDriverCwyWidth);
   if (rc) {
+    // join the side stream before reporting: its enqueued kernels may still
+    // read A / tp and write VT, which the caller frees after an error
     h->last_error = sd->last_error;
+    cudaStreamSynchronize(sd->own_stream);
     return rc;
   }
   rc = ormbr_run(h, st, 'Q', false, m, n, A, lda, tq, U, m, n, ldu, kDriverCwyWidth);
@@ -679,6 +709,13 @@ int dcsvd_gesdd_batched(dcsvd_handle h, int batch, int64_t m, int64_t n, double*
     conc = k <= 2560 ? 8 : (k <= 4096 ? 4 : (k <= 6144 ? 2 : 1));
   }
   conc = std::max(1, std::min(conc, std::min(batch, 16)));
+  {
+    // each sub-context's cooperative LABRD grid needs sms/conc >= ceil(rows/512)
+    // (gebrd.cu labrd_launch): clamp the concurrency to the GEBRD row count
+    const long long M = std::max(m, n), K = std::min(m, n);
+    const long long rows = (M >= o.ts_crossover * K && M > K) ? K : M;
+    while (conc > 1 && (long long)(h->sms / conc) * 512 < rows) --conc;
+  }
   if (conc == 1) {
     for (int b = 0; b < batch; ++b) {
       PhaseTimer pt(false, st);
@@ -711,7 +748,10 @@ int dcsvd_gesdd_batched(dcsvd_handle h, int batch, int64_t m, int64_t n, double*
         c = gesdd_impl(s, s->own_stream, m, n, A[b], lda, Sg[b], U ? U[b] : nullptr, ldu, VT ? VT[b] : nullptr,
                        ldvt, o, pt);
       }
-      if (c == 0) c = check_device_status(s, s->own_stream, "gesdd_batched");
+      if (c == 0)
+        c = check_device_status(s, s->own_stream, "gesdd_batched");
+      else
+        cudaStreamSynchronize(s->own_stream);  // no enqueued work outlives the failed call
       codes[t] = c;
     });
   }

@@ -22,6 +22,7 @@
 // partial order (bit-reproducible).  The trailing update A -= P Q^T is one
 // DMMA GEMM (gemm.cu).  The final <= nb columns use a single-CTA GEBD2.
 #include <algorithm>
+#include <mutex>
 #include <cooperative_groups.h>
 
 #include "ctx.cuh"
@@ -1165,10 +1166,17 @@ static size_t gebd2c_bytes(int m, int n, int cs, int* R, int* LD) {
 // cluster size for gebd2_cluster_kernel: 16 when the GPU can co-schedule it, else 8
 static int gebd2c_cluster_size() {
   if (g_gebd2_cluster == 8) return 8;  // debug: force the portable cluster size
-  // thread-safe one-time probe (batched SVDs call this from several host threads)
-  static const int cs = [] {
-    cudaFuncSetAttribute(gebd2_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kG2cSmemMax);
-    cudaFuncSetAttribute(gebd2_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  // per-device probe, cached; thread-safe (batched SVDs call this from several host threads)
+  static std::mutex mu;
+  static int per_dev[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  std::lock_guard<std::mutex> lk(mu);
+  if (per_dev[dev]) return per_dev[dev];
+  per_dev[dev] = [] {
+    func_attr(gebd2_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kG2cSmemMax);
+    func_attr(gebd2_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1181,7 +1189,7 @@ static int gebd2c_cluster_size() {
     cudaGetLastError();
     return ok16 ? 16 : 8;
   }();
-  return cs;
+  return per_dev[dev];
 }
 
 // Measured per-column crossover with the two-phase LABRD panels (tools/gebd2_cluster_ab.py):
@@ -1219,7 +1227,7 @@ constexpr int kLabrdSmemMax = 225 * 1024;  // 227 KB opt-in minus static shared 
 
 template <typename K>
 static int launch_coop(K kern, cudaStream_t st, LabrdArgs& la, int grid, size_t smem) {
-  DC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kLabrdSmemMax));
+  DC_CUDA_TRY((cudaError_t)func_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kLabrdSmemMax));
   void* args[] = {&la};
   DC_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(kLabrdThreads), args, smem, st));
   note_launch();

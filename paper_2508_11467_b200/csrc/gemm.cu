@@ -286,11 +286,7 @@ static int launch_cfg_v(cudaStream_t st, const GemmBatch* b, const GemmDesc* dd,
   using Cfg = GemmCfg<TA, TB, BM, BN, BK, WM, WN, STAGES>;
   auto kern = dgemm_kernel<TA, TB, BM, BN, BK, WM, WN, STAGES, MINB, PFC, VEC, GATHER>;
   constexpr int smem = Cfg::SMEM_BYTES + (PFC ? Cfg::C_ELEMS * 8 : 0);
-  static bool attr_set = false;
-  if (!attr_set) {
-    DC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr_set = true;
-  }
+  DC_CUDA_TRY((cudaError_t)func_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   dim3 grid((max_m + BM - 1) / BM, (max_n + BN - 1) / BN, nz);
   GemmBatch empty;
   empty.count = 0;
@@ -622,11 +618,7 @@ template <bool TB, int KMAX, int MT, int WARPS_M, bool VEC>
 static int launch_rankk_v(cudaStream_t st, const GemmDesc& d, int sms) {
   using Cfg = RankkCfg<TB, KMAX, MT, WARPS_M>;
   auto kern = rankk_stream_kernel<TB, KMAX, MT, WARPS_M, VEC>;
-  static bool attr = false;
-  if (!attr) {
-    DC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
-    attr = true;
-  }
+  DC_CUDA_TRY((cudaError_t)func_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
   const int strips = (d.n + 63) / 64;
   const int tiles = (d.m + MT - 1) / MT;
   const int chunk = rankk_chunk(d.m, strips, tiles, MT, KMAX, Cfg::CHUNK, sms);

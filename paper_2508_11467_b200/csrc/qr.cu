@@ -118,12 +118,8 @@ __global__ void __launch_bounds__(32 * kTinvSolveWarps) cwy_tinv_solve_kernel(co
 }
 
 static int tinv_solve_launch(cudaStream_t st, const double* Tinv, int w, bool trans, double* Top) {
-  static bool attr = false;
-  if (!attr) {
-    DC_CUDA_TRY(cudaFuncSetAttribute(cwy_tinv_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kCwyMaxW * kCwyMaxW * 8));
-    attr = true;
-  }
+  DC_CUDA_TRY((cudaError_t)func_attr(cwy_tinv_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kCwyMaxW * kCwyMaxW * 8));
   cwy_tinv_solve_kernel<<<(w + kTinvSolveWarps - 1) / kTinvSolveWarps, 32 * kTinvSolveWarps, (size_t)w * w * 8, st>>>(
       Tinv, w, trans ? 1 : 0, Top);
   note_launch();
@@ -433,11 +429,7 @@ static int geqr2_launch(dcsvd_ctx* h, cudaStream_t st, double* A, long long lda,
   const bool in_smem = sizeof(double) * (size_t)R1 * w <= 200 * 1024;
   const size_t smem = in_smem ? sizeof(double) * (size_t)R1 * w : 0;
   if (G > 160 || w > 64) return set_error(h, DCSVD_EINVAL, "QR panel kernel supports <= 160 CTAs and 64 columns");
-  static bool attr = false;
-  if (!attr) {
-    DC_CUDA_TRY(cudaFuncSetAttribute(geqr2_coop_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  DC_CUDA_TRY((cudaError_t)func_attr(geqr2_coop_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   DC_CUDA_TRY(cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned), st));
   Geqr2Args a;
   a.A = A; a.lda = lda; a.m = m; a.w = w; a.tau = tau; a.part = part; a.rowbuf = part + (size_t)2 * G * 64;

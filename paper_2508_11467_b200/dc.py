@@ -75,6 +75,7 @@ class SubproblemSVD:
         return int(self.dvals.shape[0])
 
 
+@_lib.on_input_device
 def bdsdc(prob, want_vectors=True, leaf=32, tol_multiple=8.0):
     """SVD of a bidiagonal problem by divide and conquer on the GPU
     (bdc.py:861-880).  Values descending; values-only runs are bitwise equal
@@ -138,6 +139,7 @@ def _sys_vectors(system):
     return d, z, torch_in
 
 
+@_lib.on_input_device
 def solve_all_roots(system, max_iterations=100):
     """All roots of the secular system, one warp per root (bdc.py:515-641).
     Frozen-lane iteration: each root's result is independent of the others."""
@@ -158,12 +160,14 @@ def solve_all_roots(system, max_iterations=100):
     return SecularRoots(om.cpu().numpy(), anc.cpu().numpy().astype(np.intp), mu.cpu().numpy())
 
 
+@_lib.on_input_device
 def solve_secular(system, i, max_iterations=100):
     """Root i as (omega, anchor, mu) (bdc.py:528-538); bitwise the batched lane."""
     r = solve_all_roots(system, max_iterations)
     return float(r.omega[i]), int(r.anchor[i]), float(r.mu[i])
 
 
+@_lib.on_input_device
 def recompute_z(system, roots):
     """Loewner update vector consistent with the roots (bdc.py:644-673)."""
     d, z, torch_in = _sys_vectors(system)
@@ -179,6 +183,7 @@ def recompute_z(system, roots):
     return zt if torch_in else zt.cpu().numpy()
 
 
+@_lib.on_input_device
 def secular_vectors(system, roots, ztilde):
     """(umat, vmat) singular vectors of the middle matrix (bdc.py:676-694)."""
     d, _, torch_in = _sys_vectors(system)
@@ -211,6 +216,7 @@ def split(prob):
     return left, right, float(prob.d[k - 1]), float(prob.e[k - 1])
 
 
+@_lib.on_input_device
 def bdsqr_base(prob, want_vectors=True):
     """Leaf SVD by implicit-shift QR iteration (bdc.py:315-359), values
     ascending (the tree-internal convention).  n <= 32 runs the GPU leaf
@@ -272,6 +278,7 @@ def _edge_dev(edge):
     return t
 
 
+@_lib.on_input_device
 def build_z(node, left, right):
     """Middle-row data of a merge (bdc.py:382-412): (d, z, coupling) in
     pre-sort order [border, left child values, right child values]; coupling
@@ -336,6 +343,7 @@ class _InPlace:
             x[...] = _lib.to_host(self.dev)
 
 
+@_lib.on_input_device
 def deflate(d, z, left_vectors=None, right_vectors=None, *, edge_rows=None, left_classes=None, right_classes=None,
             tol_multiple=8.0):
     """Sort the merge entries and deflate the negligible ones (bdc.py:423-508).
@@ -442,6 +450,7 @@ def ctypes_offset(t, row, col=0):
     return ctypes.c_void_p(t.data_ptr() + 8 * (row + col * _lib.ld(t)))
 
 
+@_lib.on_input_device
 def merge_vectors(outcome, umat, vmat, left, right, left_classes, right_classes, mid_row):
     """Assemble a merged node's vector columns (bdc.py:731-747): kept columns
     through the structured DMMA products, deflated columns carried over.

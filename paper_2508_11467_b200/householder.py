@@ -57,6 +57,7 @@ def _writeback(orig, dev, was_np):
     return dev
 
 
+@_lib.on_input_device
 def geqrf_blocked(a, block=32):
     """Blocked Householder QR in place (qrblock.py:122-144): cooperative
     shared-memory panel kernel + CWY trailing update."""
@@ -77,6 +78,7 @@ def geqrf_blocked(a, block=32):
     return QRFactorization(packed, tau.cpu().numpy() if was_np else tau)
 
 
+@_lib.on_input_device
 def orgqr(fact, k, block=64):
     """First k columns of Q = H_1...H_n (qrblock.py:147-164)."""
     m, n = fact.shape
@@ -107,6 +109,7 @@ def _apply(seq, c, vect, transpose, block):
     return _writeback(c, C, c_np)
 
 
+@_lib.on_input_device
 def ormqr_like(seq, c, transpose=False, block=64):
     """C <- U1 C (or U1^T C) with the left (column) reflectors
     (backtransform.py:90-109)."""
@@ -121,6 +124,7 @@ def ormqr_like(seq, c, transpose=False, block=64):
     return _apply(seq, c, "Q", transpose, block)
 
 
+@_lib.on_input_device
 def ormlq_like(seq, c, transpose=False, block=64):
     """C <- C V1 (or C V1^T) with the right (row) reflectors
     (backtransform.py:112-131)."""
@@ -141,6 +145,7 @@ class CompactWYBlock:
     tinv: object
 
 
+@_lib.on_input_device
 def build_tinv(y, tau):
     """Tinv = strict-upper(Y^T Y) + diag(1/tau) (1 for tau == 0)
     (qrblock.py:90-100): one DMMA GEMM + one kernel."""
@@ -169,6 +174,7 @@ def _apply_block(block, c, transpose, side):
     return _writeback(c, C, c_np)
 
 
+@_lib.on_input_device
 def apply_block_reflector_left(block, c, transpose=False):
     """C <- (I - Y T Y^T) C, or the transposed block (qrblock.py:103-111)."""
     if c.shape[0] != block.y.shape[0]:
@@ -176,6 +182,7 @@ def apply_block_reflector_left(block, c, transpose=False):
     return _apply_block(block, c, transpose, "L")
 
 
+@_lib.on_input_device
 def apply_block_reflector_right(block, c, transpose=False):
     """C <- C (I - Y T Y^T), or the transposed block (qrblock.py:114-119)."""
     if c.shape[1] != block.y.shape[0]:
@@ -183,6 +190,7 @@ def apply_block_reflector_right(block, c, transpose=False):
     return _apply_block(block, c, transpose, "R")
 
 
+@_lib.on_input_device
 def geqrf_panel(a, tau):
     """Unblocked Householder QR of a tall panel in place (qrblock.py:51-71);
     cooperative kernel with the panel's row slabs in shared memory."""

@@ -103,6 +103,7 @@ def _run(a, options, prof):
     return res, pt
 
 
+@_lib.on_input_device
 def gesdd(a, options=None):
     """Economy SVD A = U diag(sigma) Vt on the GPU (driver.py:147-157).
     The input is not modified."""
@@ -112,6 +113,7 @@ def gesdd(a, options=None):
 svd = gesdd
 
 
+@_lib.on_input_device
 def phase_profile(a, options=None):
     """gesdd with per-phase device time attribution (driver.py:160-170)."""
     _, pt = _run(a, options, True)
@@ -120,6 +122,7 @@ def phase_profile(a, options=None):
     return PhaseProfile(phases, pt.total)
 
 
+@_lib.on_input_device
 def gesdd_batched(mats, options=None, concurrency=0):
     """Independent SVDs of a list of equally shaped matrices (BASELINE
     config 5).  Device tensors in -> device tensors out; numpy -> numpy."""

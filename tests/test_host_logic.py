@@ -126,6 +126,63 @@ def test_batch_gather_two_ranks_gloo():
     assert order == [float(i) for i in range(10)]
 
 
+def _gloo_sigma_worker(rank, ws, port, q):
+    import torch.distributed as dist
+
+    from paper_2508_11467_b200.batch import gather_sigma, shard_range
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    total, k = 11, 4
+    lo, hi = shard_range(total, ws, rank)
+    local = torch.stack([torch.arange(k, dtype=torch.float64) + 10.0 * i for i in range(lo, hi)])
+    full = gather_sigma(local, total)
+    q.put((rank, full.numpy().tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ws", [2, 3])
+def test_gather_sigma_gloo(ws):
+    """batch.gather_sigma (the C5 sigma gather) at world size 2 and 3 with
+    uneven shards: every rank gets the rows in global batch order."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_sigma_worker, args=(r, ws, port, q)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(ws)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    want = [[10.0 * i + j for j in range(4)] for i in range(11)]
+    for _, rows in got:
+        assert rows == want
+
+
+def test_bench_spawns_ranks_for_gpus_flag(monkeypatch):
+    """`bench.py --gpus N` outside torchrun re-launches itself under
+    torch.distributed.run with N ranks on 127.0.0.1 (bench.maybe_spawn)."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import bench
+
+    calls = []
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: calls.append(cmd) or 0)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--workload", "c5"])
+    args = type("A", (), {"gpus": 4})()
+    assert bench.maybe_spawn(args) == 0
+    cmd = calls[0]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1" and cmd[-2:] == ["--workload", "c5"]
+    monkeypatch.setenv("WORLD_SIZE", "4")
+    assert bench.maybe_spawn(args) is None
+
+
 # the `dcsvd` shim (INTEGRATION.md §4): reference module layout -> this package
 REFERENCE_ALL = (  # pkg/src/dcsvd/__init__.py:87-129
     "AccuracyReport BidiagonalFactorization BidiagonalProblem CompactWYBlock ConvergenceError DeflationOutcome "
