@@ -28,6 +28,8 @@ int set_rankk_bulk(int on);
 int set_rankk_min(long long mn);
 extern bool g_labrd_last_two_phase;
 extern int g_gemm_route;
+extern int g_rankk_ws;
+int set_ws_flags(int f);
 thread_local dcsvd_ctx* t_cur = nullptr;
 
 int func_attr(const void* fn, int attr, int value) {
@@ -386,6 +388,11 @@ int dcsvd_debug_gemm_route(int mode) {
   return 0;
 }
 
+int dcsvd_debug_ws_flags(int f) { return dc::set_ws_flags(f); }
+int dcsvd_debug_rankk_ws(int on) {
+  dc::g_rankk_ws = on;
+  return 0;
+}
 int dcsvd_debug_labrd_variant(void) { return dc::g_labrd_last_two_phase ? 2 : 4; }
 
 /* GEBD2 tail on one thread-block cluster (1, default; 8 = force 8-CTA clusters) or the panel path only (0); debug */

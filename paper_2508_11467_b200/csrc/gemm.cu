@@ -1,4 +1,7 @@
 // DMMA GEMM kernels (see gemm.cuh).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <unordered_map>
 #include <vector>
@@ -556,6 +559,320 @@ __global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P, int ch
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialized rank-k update (same contract as rankk_stream_kernel, for
+// operands whose leading dimensions / bases allow 2-D TMA tensor maps): one
+// producer warp (one elected lane) moves every operand with TMA tensor copies
+// (cp.async.bulk.tensor.2d, SASS UTMALDG) -- ONE instruction per A tile and
+// per B strip -- into a ring of S A-tile stages and a B-strip buffer, each
+// completing on its own "full" mbarrier, and prefetches the tile's C block
+// into L2 with one cp.async.bulk.prefetch.tensor.  The boxes are 4 elements
+// wider than the tile along the contiguous dimension, so the shared-memory
+// pitch is 4 mod 16 doubles and the m8n8k4 fragment reads stay bank-conflict
+// free (the 4 extra rows are ignored; out-of-range elements are zero-filled
+// by the TMA unit, which also supplies the K -> multiple-of-4 padding).
+// NG consumer groups of 4 warps (one warp per SM sub-partition) take the
+// row tiles of a unit round-robin and run only LDS + DMMA, release the A
+// stage on its "empty" mbarrier after their last fragment read, then do the
+// C read-modify-write epilogue.  The groups never synchronise with each
+// other, so one group's epilogue / stage wait overlaps the other's DMMAs (the
+// per-tile CTA barriers are what kept rankk_stream_kernel at ~60 % DMMA-pipe
+// activity), and the producer's copy issue is off the math warps entirely
+// (per-column 1-D bulk copies from one warp were issue-bound: 13 TF/s).
+int rankk_chunk(int m, int strips, int tiles, int mt, int kmax, int cmax, int sms);
+__constant__ int g_ws_flags = 0;  // debug: bit 0 = no C prefetch
+int set_ws_flags(int f) { return cudaMemcpyToSymbol(g_ws_flags, &f, sizeof(int)) == cudaSuccess ? 0 : -1; }
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst), b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+      ::"r"(d), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(b) : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1) : "memory");
+}
+
+template <bool TB, int KMAX, int MT, int NG, int S>
+struct RankkWsCfg {
+  static constexpr int NW = 64;
+  static constexpr int THREADS = 32 + 128 * NG;
+  static constexpr int WARPS_M = MT >= 32 ? 2 : 1, WARPS_N = 4 / WARPS_M;  // per group
+  static constexpr int WTM = MT / WARPS_M, WTN = NW / WARPS_N;
+  static constexpr int FM = WTM / 8, FN = WTN / 8;
+  static constexpr int LDA_S = MT + 4;  // [k][m]: TMA box {MT + 4, Kp}
+  static constexpr int A_ELEMS = KMAX * LDA_S;
+  static constexpr int LDB_S = TB ? (NW + 4) : (KMAX + 4);  // box {68, Kp} or {KMAX + 4, 64}
+  static constexpr int B_ELEMS = TB ? KMAX * LDB_S : NW * LDB_S;
+  static constexpr int NBUF = 2;  // B strips double-buffered: the groups flow across unit boundaries
+  static constexpr int SMEM_BYTES = (NBUF * B_ELEMS + S * A_ELEMS) * 8 + 128;  // +128: manual alignment
+  static constexpr int CHUNK = 64;
+};
+
+__device__ __forceinline__ double neg_bits(double x) {  // -x on the integer pipe (not a DADD)
+  double r;
+  asm("{\n.reg .b32 lo, hi;\nmov.b64 {lo, hi}, %1;\nxor.b32 hi, hi, 0x80000000;\nmov.b64 %0, {lo, hi};\n}"
+      : "=d"(r) : "d"(x));
+  return r;
+}
+
+template <bool TB, int KMAX, int MT, int NG, int S>
+__global__ void __launch_bounds__(32 + 128 * NG, 1)
+    rankk_ws_kernel(GemmDesc P, int chunk, const __grid_constant__ CUtensorMap tA,
+                    const __grid_constant__ CUtensorMap tB, const __grid_constant__ CUtensorMap tC) {
+  using Cfg = RankkWsCfg<TB, KMAX, MT, NG, S>;
+  constexpr int NW = Cfg::NW;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // 128-byte alignment by pointer arithmetic (keeps the shared address space: LDS, not generic LD)
+  double* Bs = reinterpret_cast<double*>(smem_raw + ((128u - ((unsigned)__cvta_generic_to_shared(smem_raw) & 127u)) & 127u));
+  double* As = Bs + Cfg::NBUF * Cfg::B_ELEMS;
+  __shared__ __align__(8) uint64_t a_full[S], a_empty[S], b_full[Cfg::NBUF], b_empty[Cfg::NBUF];
+  const int M = P.m, N = P.n, K = P.k;
+  double* __restrict__ C = P.C;
+  const long long ldc = P.ldc;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int Kp = (K + 3) & ~3;
+  const int strips = (N + NW - 1) / NW;
+  const int tiles = (M + MT - 1) / MT;
+  const int chunks = (tiles + chunk - 1) / chunk;
+  const int units = strips * chunks;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&a_full[s], 1);
+      mbar_init(&a_empty[s], 4);
+    }
+    for (int b = 0; b < Cfg::NBUF; ++b) {
+      mbar_init(&b_full[b], 1);
+      mbar_init(&b_empty[b], 4 * NG);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ------------------------------ producer (one lane)
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tB)) : "memory");
+      const unsigned a_bytes = (unsigned)(Cfg::LDA_S * Kp * 8);
+      const unsigned b_bytes = (unsigned)((TB ? Cfg::LDB_S * Kp : Cfg::LDB_S * NW) * 8);
+      const bool pfc = P.beta != 0.0 && !(g_ws_flags & 1);
+      unsigned seq = 0, useq = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++useq) {
+        const int n0 = (u / chunks) * NW;
+        const int t0 = (u % chunks) * chunk, t1 = min(tiles, t0 + chunk);
+        const int bb = useq % Cfg::NBUF;
+        if (useq >= (unsigned)Cfg::NBUF) mbar_wait(&b_empty[bb], ((useq / Cfg::NBUF) - 1) & 1u);
+        mbar_expect_tx(&b_full[bb], b_bytes);
+        if (TB) tma_load_2d(Bs + bb * Cfg::B_ELEMS, &tB, n0, 0, &b_full[bb]);
+        else tma_load_2d(Bs + bb * Cfg::B_ELEMS, &tB, 0, n0, &b_full[bb]);
+        for (int t = t0; t < t1; ++t, ++seq) {
+          const int st = seq % S;
+          if ((g_ws_flags & 4) && seq >= (unsigned)S) continue;  // debug: stages loaded once
+          if (seq >= (unsigned)S) mbar_wait(&a_empty[st], ((seq / S) - 1) & 1u);
+          mbar_expect_tx(&a_full[st], a_bytes);
+          tma_load_2d(As + st * Cfg::A_ELEMS, &tA, t * MT, 0, &a_full[st]);
+          if (pfc) tma_prefetch_2d(&tC, t * MT, n0);
+        }
+      }
+    }
+    return;
+  }
+  // ------------------------------ consumers
+  const double* smem_b = Bs;
+  const int ct = tid - 32;
+  const int grp = ct >> 7;       // consumer group
+  const int gw = (ct >> 5) & 3;  // warp within the group
+  const int wm = gw % Cfg::WARPS_M, wn = gw / Cfg::WARPS_M;
+  const int lr = lane >> 2, lc = lane & 3;
+  const double alpha = P.alpha, beta = P.beta;
+  // C -= A op(B) (alpha = -1, beta = 1: every rank-k update of the pipeline) and
+  // C += A op(B): the accumulators start from the C fragment (C -= AB runs as
+  // -((-C) + AB), the sign flips by integer XORs on the load and the store),
+  // so the epilogue is plain stores -- no FP64 instruction competes with the
+  // DMMAs for the shared FP64/tensor pipe.  Other (alpha, beta): general epilogue.
+  const bool fold = beta == 1.0 && (alpha == 1.0 || alpha == -1.0);
+  const bool noc = g_ws_flags & 2;  // debug: no C traffic (pipeline bound)
+  const bool negb = alpha == -1.0;
+  unsigned seqb = 0, useq = 0;
+  double cn[Cfg::FM][Cfg::FN][2];
+  bool have_next = false;
+  for (int u = blockIdx.x; u < units; u += gridDim.x, ++useq) {
+    const int n0 = (u / chunks) * NW;
+    const int t0 = (u % chunks) * chunk, t1 = min(tiles, t0 + chunk);
+    auto load_c = [&](int tt, double (&dst)[Cfg::FM][Cfg::FN][2]) {
+      const int mm = tt * MT;
+      const bool fl = mm + MT <= M && n0 + NW <= N;
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gn = n0 + wn * Cfg::WTN + j * 8 + lc * 2 + h;
+          const double* cc = C + (long long)gn * ldc + mm + wm * Cfg::WTM + lr;
+#pragma unroll
+          for (int i = 0; i < Cfg::FM; ++i)
+            dst[i][j][h] = (fl || (gn < N && mm + wm * Cfg::WTM + i * 8 + lr < M)) ? __ldcg(cc + i * 8) : 0.0;
+        }
+    };
+    have_next = false;
+    const int bb = useq % Cfg::NBUF;
+    mbar_wait(&b_full[bb], (useq / Cfg::NBUF) & 1u);
+    const double* Bs = smem_b + bb * Cfg::B_ELEMS;
+    for (int t = t0 + grp; t < t1; t += NG) {
+      const unsigned seq = seqb + (unsigned)(t - t0);
+      const int st = seq % S;
+      const int m0 = t * MT;
+      const bool full = m0 + MT <= M && n0 + NW <= N;  // no bounds predicates
+      double acc[Cfg::FM][Cfg::FN][2];
+      if (fold && !noc) {
+        // C fragment (L2-prefetched by the producer) as the accumulator init;
+        // the group's next tile of the unit is loaded now into cn, one tile
+        // ahead of its use, so only a unit's first tile waits on C
+        if (!have_next) load_c(t, cn);
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < Cfg::FN; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) acc[i][j][h] = negb ? neg_bits(cn[i][j][h]) : cn[i][j][h];
+        have_next = t + NG < t1;
+        if (have_next) load_c(t + NG, cn);
+      } else {
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      }
+      if (!(g_ws_flags & 4) || seq < (unsigned)S) mbar_wait(&a_full[st], (seq / S) & 1u);
+      const double* as = As + st * Cfg::A_ELEMS;
+#pragma unroll 4
+      for (int ks = 0; ks < Kp; ks += 4) {
+        double af[Cfg::FM], bf[Cfg::FN];
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i) af[i] = as[(ks + lc) * Cfg::LDA_S + wm * Cfg::WTM + i * 8 + lr];
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) {
+          const int n = wn * Cfg::WTN + j * 8 + lr;
+          bf[j] = TB ? Bs[(ks + lc) * Cfg::LDB_S + n] : Bs[n * Cfg::LDB_S + ks + lc];
+        }
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < Cfg::FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+      __syncwarp();
+      if (lane == 0 && !(g_ws_flags & 4)) mbar_arrive(&a_empty[st]);
+      if (fold) {
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int gn = n0 + wn * Cfg::WTN + j * 8 + lc * 2 + h;
+            double* cc = C + (long long)gn * ldc + m0 + wm * Cfg::WTM + lr;
+#pragma unroll
+            for (int i = 0; i < Cfg::FM; ++i)
+              if ((full || (gn < N && m0 + wm * Cfg::WTM + i * 8 + lr < M)) && (!noc || acc[i][j][h] == 1.2345e300))
+                cc[i * 8] = negb ? neg_bits(acc[i][j][h]) : acc[i][j][h];
+          }
+        continue;
+      }
+      // general (alpha, beta): C read after the math, in two halves of the column
+      // blocks (bounded registers); every load of a half in flight before its stores
+      constexpr int EPI = Cfg::FN >= 2 ? 2 : 1;
+#pragma unroll
+      for (int e = 0; e < EPI; ++e) {
+        double cv[Cfg::FM][Cfg::FN / EPI][2];
+#pragma unroll
+        for (int jj = 0; jj < Cfg::FN / EPI; ++jj)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int gn = n0 + wn * Cfg::WTN + (e * (Cfg::FN / EPI) + jj) * 8 + lc * 2 + h;
+#pragma unroll
+            for (int i = 0; i < Cfg::FM; ++i) {
+              const int gm = m0 + wm * Cfg::WTM + i * 8 + lr;
+              cv[i][jj][h] = (beta != 0.0 && gn < N && gm < M) ? __ldcg(C + (long long)gm + (long long)gn * ldc) : 0.0;
+            }
+          }
+#pragma unroll
+        for (int jj = 0; jj < Cfg::FN / EPI; ++jj) {
+          const int j = e * (Cfg::FN / EPI) + jj;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int gn = n0 + wn * Cfg::WTN + j * 8 + lc * 2 + h;
+            if (gn >= N) continue;
+            double* cc = C + (long long)gn * ldc;
+#pragma unroll
+            for (int i = 0; i < Cfg::FM; ++i) {
+              const int gm = m0 + wm * Cfg::WTM + i * 8 + lr;
+              if (gm < M) cc[gm] = alpha * acc[i][j][h] + beta * cv[i][jj][h];
+            }
+          }
+        }
+      }
+    }
+    seqb += (unsigned)(t1 - t0);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&b_empty[bb]);  // this warp is done with the unit's B strip
+  }
+}
+
+int g_rankk_ws = 1;  // debug: 0 = rankk_stream_kernel only
+
+// 2-D fp64 tensor map: `inner` contiguous elements per line, `outer` lines
+// `ld` elements apart; box {box_inner, box_outer}; out-of-range -> zero.
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+int make_tmap_2d(CUtensorMap* map, const double* base, long long inner, long long outer, long long ld,
+                 int box_inner, int box_outer) {
+  auto fn = tmap_encode_fn();
+  if (!fn) return -1;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -1;
+}
+
+template <bool TB, int KMAX, int MT, int NG, int S>
+static int launch_rankk_ws(cudaStream_t st, const GemmDesc& d, int sms, int kmax_cost) {
+  using Cfg = RankkWsCfg<TB, KMAX, MT, NG, S>;
+  const int Kp = (d.k + 3) & ~3;
+  CUtensorMap tA, tB, tC;
+  if (make_tmap_2d(&tA, d.A, d.m, d.k, d.lda, Cfg::LDA_S, Kp)) return -1;
+  if (TB) {
+    if (make_tmap_2d(&tB, d.B, d.n, d.k, d.ldb, Cfg::LDB_S, Kp)) return -1;
+  } else if (make_tmap_2d(&tB, d.B, d.k, d.n, d.ldb, Cfg::LDB_S, Cfg::NW)) {
+    return -1;
+  }
+  if (make_tmap_2d(&tC, d.C, d.m, d.n, d.ldc, MT, Cfg::NW)) return -1;
+  auto kern = rankk_ws_kernel<TB, KMAX, MT, NG, S>;
+  DC_CUDA_TRY((cudaError_t)func_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+  const int strips = (d.n + 63) / 64;
+  const int tiles = (d.m + MT - 1) / MT;
+  // at least one tile per consumer group in a unit (the groups share its B strip)
+  const int chunk =
+      std::min(tiles, std::max(NG, rankk_chunk(d.m, strips, tiles, MT, kmax_cost, Cfg::CHUNK, sms)));
+  const int units = strips * ((tiles + chunk - 1) / chunk);
+  const int grid = std::max(1, std::min(units, sms));
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(d, chunk, tA, tB, tC);
+  note_launch();
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 // Row tiles per work unit.  The CTAs take units round-robin, so the kernel's
 // time is the largest per-CTA sum of unit costs: the unit's rows in tiles
 // (the last tile may be short) plus a fixed start cost `s` for loading its B
@@ -576,7 +893,7 @@ int set_rankk_chunk(int c) {
   g_rankk_chunk = c;
   return 0;
 }
-static int rankk_chunk(int m, int strips, int tiles, int mt, int kmax, int cmax, int sms) {
+int rankk_chunk(int m, int strips, int tiles, int mt, int kmax, int cmax, int sms) {
   if (g_rankk_chunk > 0) return std::min(g_rankk_chunk, cmax);
   const unsigned long long key = ((unsigned long long)m << 40) ^ ((unsigned long long)strips << 20) ^
                                  ((unsigned long long)kmax << 8) ^ (unsigned long long)sms;
@@ -656,6 +973,18 @@ static int try_rankk(cudaStream_t st, bool ta, bool tb, const GemmDesc& d) {
   if (ta || d.acol || d.ccol || d.k < 1 || d.k > 128 || d.beta == 0.0) return -1;
   if ((long long)d.m * d.n < g_rankk_min_mn || d.m < 256) return -1;
   const int sms = sm_count();
+  // TMA tensor maps need 16-byte-aligned bases and leading dimensions.  The
+  // warp-specialized kernel wins for K > 64 (8192^2 K = 128: 24.0 -> 24.9
+  // TFLOP/s, C2 ORMBR 90.0 -> 87.3 ms); at K <= 64 (GEBRD trailing update)
+  // the streaming kernel stays ahead (21.6 vs 19.9 at 8160^2), see DESIGN.md.
+  const bool ws_ok = g_rankk_ws && d.k > 64 &&
+                     !((reinterpret_cast<uintptr_t>(d.A) & 15) || (reinterpret_cast<uintptr_t>(d.B) & 15) ||
+                       (reinterpret_cast<uintptr_t>(d.C) & 15) || (d.lda & 1) || (d.ldb & 1) || (d.ldc & 1));
+  if (ws_ok) {
+    const int r = tb ? launch_rankk_ws<true, 128, 16, 3, 4>(st, d, sms, 64)
+                     : launch_rankk_ws<false, 128, 16, 3, 4>(st, d, sms, 64);
+    if (r >= 0) return r;  // -1: tensor map not encodable -> streaming kernel
+  }
   if (d.k <= 64) return tb ? launch_rankk<true, 64, 128, 4>(st, d, sms) : launch_rankk<false, 64, 128, 4>(st, d, sms);
   return tb ? launch_rankk<true, 128, 64, 2>(st, d, sms) : launch_rankk<false, 128, 64, 2>(st, d, sms);
 }

@@ -426,21 +426,45 @@ def test_c2_scale_square_8192(cuda):
 @pytest.mark.parametrize("k", [1, 37, 64, 100, 128])
 @pytest.mark.parametrize("tb", [False, True])
 @pytest.mark.parametrize("m", [2000, 2001])
-def test_rank_k_update_kernel(cuda, k, tb, m):
-    """Large rank-k updates take the streaming kernel (gemm.cu); compare with
-    a plain torch fp64 product.  m = 2001 leaves an odd-row last tile, which
-    takes the cp.async fallback next to the TMA bulk-copied tiles."""
+@pytest.mark.parametrize("ab", [(-1.0, 0.75), (-1.0, 1.0), (1.0, 1.0)])
+def test_rank_k_update_kernel(cuda, k, tb, m, ab):
+    """Large rank-k updates take the streaming kernel (K <= 64) or the
+    warp-specialized TMA tensor-map kernel (K > 64; gemm.cu); compare with a
+    plain torch fp64 product.  m = 2001 leaves an odd-row last tile (cp.async
+    fallback / TMA zero fill).  (alpha, beta) = (+-1, 1) takes the folded
+    accumulator path of the TMA kernel, others its general epilogue."""
     g = _g()
+    alpha, beta = ab
     torch.manual_seed(k)
     n = 1500
     a = torch.randn(m, k, dtype=torch.float64, device=cuda)
     b = torch.randn(n, k, dtype=torch.float64, device=cuda) if tb else torch.randn(k, n, dtype=torch.float64, device=cuda)
     c = torch.randn(n, m, dtype=torch.float64, device=cuda).t()  # column-major m x n
-    ref = 0.75 * c + (-1.0) * (a @ (b.t() if tb else b))
+    ref = beta * c + alpha * (a @ (b.t() if tb else b))
     a_cm = a.t().contiguous().t()
     b_cm = b.t().contiguous().t()
-    g.matmul_accumulate(-1.0, a_cm, False, b_cm, tb, 0.75, c)
+    g.matmul_accumulate(alpha, a_cm, False, b_cm, tb, beta, c)
     assert (c - ref).abs().max().item() <= 1e-12 * max(k, 1)
+
+
+@pytest.mark.parametrize("ws", [0, 1])
+def test_rank_k_kernels_agree_on_pipeline_shapes(cuda, ws):
+    """The ORMBR-shaped rank-128 update (8192 x 4096, C -= Y X) through both
+    rank-k kernels (dcsvd_debug_rankk_ws) against torch."""
+    g = _g()
+    lib = _lib_handle()
+    torch.manual_seed(5)
+    m, n, k = 8192, 4096, 128
+    a = torch.randn(k, m, dtype=torch.float64, device=cuda).t()
+    b = torch.randn(n, k, dtype=torch.float64, device=cuda).t()
+    c = torch.randn(n, m, dtype=torch.float64, device=cuda).t()
+    ref = c - a @ b
+    lib.dcsvd_debug_rankk_ws(ws)
+    try:
+        g.matmul_accumulate(-1.0, a, False, b, False, 1.0, c)
+    finally:
+        lib.dcsvd_debug_rankk_ws(1)
+    assert (c - ref).abs().max().item() <= 1e-12 * k
 
 
 def test_gesdd_batched_high_concurrency(cuda):
