@@ -29,6 +29,7 @@ int set_rankk_min(long long mn);
 extern bool g_labrd_last_two_phase;
 extern int g_gemm_route;
 extern int g_rankk_ws;
+int g_ts_literal = 1;  // TS recombination: 1 = ORGQR + GEMM (driver.py:141-142), 0 = fused reflector apply
 int set_ws_flags(int f);
 thread_local dcsvd_ctx* t_cur = nullptr;
 
@@ -299,8 +300,10 @@ int gesdd_tall(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* 
                double* U, long long ldu, double* VT, long long ldvt, const dcsvd_opts& o, PhaseTimer& pt) {
   const bool vec = o.want_vectors != 0;
   const bool ts = (double)m >= o.ts_crossover * (double)n && m > n;
+  const bool literal = ts && vec && g_ts_literal;
   size_t need = pool_bytes(4 * n + 8, 8);
   if (ts) need += pool_bytes(n, 8) + pool_bytes((size_t)n * n, 8);
+  if (literal) need += pool_bytes((size_t)n * n, 8) + pool_bytes((size_t)m * n, 8);
   int rc = pool_reserve(h, 1, need, st);
   if (rc) return rc;
   double* dbuf = pool_take<double>(h, 1, 4 * n + 8);
@@ -313,13 +316,26 @@ int gesdd_tall(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* 
   if (rc) return rc;
   triu_copy_kernel<<<std::min<long long>(148 * 8, (n * n + 255) / 256), 256, 0, st>>>((int)n, A, lda, R, n);
   note_launch();
+  if (literal) {
+    // the reference's own order (driver.py:133-142): core SVD of R -> U0;
+    // Q = orgqr(QR, n) (m x n, 128-wide CWY blocks); U = Q U0 (one DMMA GEMM)
+    double* U0 = pool_take<double>(h, 1, (size_t)n * n);
+    double* Qw = pool_take<double>(h, 1, (size_t)m * n);
+    rc = square_core(h, st, n, n, R, n, S, U0, n, VT, ldvt, o, pt, dbuf);
+    if (rc) return rc;
+    pt.mark(PH_ORGQR);
+    rc = orgqr_run(h, st, m, n, n, A, lda, tau, Qw, m, kDriverCwyWidth);
+    if (rc) return rc;
+    pt.mark(PH_GEMM);
+    GemmDesc gd{(int)m, (int)n, (int)n, Qw, m, nullptr, U0, n, U, ldu, nullptr, 1.0, 0.0};
+    return gemm_launch(st, false, false, gd);
+  }
   // the core SVD of R writes its left vectors U0 straight into the top n rows of U
   rc = square_core(h, st, n, n, R, n, S, vec ? U : nullptr, ldu, VT, ldvt, o, pt, dbuf);
   if (rc || !vec) return rc;
-  // Recombination U = Q [U0; 0] (driver.py:141-142 forms Q = orgqr(...) and
-  // multiplies): applying the n QR reflectors to [U0; 0] in 128-wide CWY
-  // blocks is the same product with 4mn^2 - 2n^3 flops instead of
-  // 4mn^2 - 4n^3/3 (ORGQR) + 2mn^2 (GEMM), and needs no m x n Q.
+  // Fused recombination (dcsvd_debug_ts_literal(0)): U = Q [U0; 0] as the n QR
+  // reflectors applied to [U0; 0] in 128-wide CWY blocks -- the same product
+  // with 4mn^2 - 2n^3 flops and no m x n Q.
   pt.mark(PH_GEMM);
   if (m > n) DC_CUDA_TRY(cudaMemset2DAsync(U + n, sizeof(double) * ldu, 0, sizeof(double) * (m - n), n, st));
   return ormbr_run(h, st, 'Q', false, m, n, A, lda, tau, U, m, n, ldu, kDriverCwyWidth);
@@ -388,6 +404,10 @@ int dcsvd_debug_gemm_route(int mode) {
   return 0;
 }
 
+int dcsvd_debug_ts_literal(int on) {
+  dc::g_ts_literal = on;
+  return 0;
+}
 int dcsvd_debug_ws_flags(int f) { return dc::set_ws_flags(f); }
 int dcsvd_debug_rankk_ws(int on) {
   dc::g_rankk_ws = on;
