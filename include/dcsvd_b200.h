@@ -162,9 +162,11 @@ int dcsvd_block_reflector(dcsvd_handle h, char side, int trans, int64_t rows_y, 
 /* geqrf_panel (qrblock.py:51-71): unblocked QR of an m x w panel in place, w <= 64. */
 int dcsvd_geqrf_panel(dcsvd_handle h, int64_t m, int w, double* A, int64_t lda, double* tau, void* stream);
 /* solve_all_roots (bdc.py:515-641) of one secular system (d ascending, d[0] = 0):
- * omega[K], anchor[K] (int32), mu[K]. */
+ * omega[K], anchor[K] (int32), mu[K]; max_iterations = the reference's budget
+ * (100 in bdsdc); a root not converged within it -> DCSVD_ENOCONV
+ * (ConvergenceError, bdc.py:636-639). */
 int dcsvd_secular_roots(dcsvd_handle h, int K, const double* d, const double* z, double* omega,
-                        int* anchor, double* mu, void* stream);
+                        int* anchor, double* mu, int max_iterations, void* stream);
 /* recompute_z (bdc.py:644-673): Loewner update vector ztilde[K]. */
 int dcsvd_recompute_z(dcsvd_handle h, int K, const double* d, const double* z, const int* anchor,
                       const double* mu, double* ztilde, void* stream);

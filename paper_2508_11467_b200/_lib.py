@@ -95,7 +95,7 @@ def load_library(path=None):
             "dcsvd_build_tinv": (I, [V, I64, I, V, I64, V, V, I64, V]),
             "dcsvd_block_reflector": (I, [V, C, I, I64, I, V, I64, V, I64, V, I64, I64, V]),
             "dcsvd_geqrf_panel": (I, [V, I64, I, V, I64, V, V]),
-            "dcsvd_secular_roots": (I, [V, I, V, V, V, V, V, V]),
+            "dcsvd_secular_roots": (I, [V, I, V, V, V, V, V, I, V]),
             "dcsvd_recompute_z": (I, [V, I, V, V, V, V, V, V]),
             "dcsvd_secular_vectors": (I, [V, I, V, V, V, V, V, I64, V, I64, V]),
             "dcsvd_build_z": (I, [V, I, I, I, D, D, V, V, I64, V, V, I64, V, V, V, V]),

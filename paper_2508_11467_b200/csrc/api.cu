@@ -841,10 +841,10 @@ int dcsvd_geqrf_panel(dcsvd_handle h, int64_t m, int w, double* A, int64_t lda, 
 }
 
 int dcsvd_secular_roots(dcsvd_handle h, int K, const double* d, const double* z, double* omega, int* anchor,
-                        double* mu, void* stream) {
+                        double* mu, int max_iterations, void* stream) {
   Guard g(h);
   if (!h) return DCSVD_EINVAL;
-  int rc = secular_run(h, S(stream), K, d, z, omega, anchor, mu);
+  int rc = secular_run(h, S(stream), K, d, z, omega, anchor, mu, max_iterations);
   if (rc) return rc;
   return check_device_status(h, S(stream), "solve_all_roots");
 }

@@ -709,7 +709,8 @@ constexpr int kSecWarps = 8;
 // One root of the secular equation per warp (all lanes participate; lane 0
 // stores).  d ascending with d[0] = 0, z, zz = sum z^2.
 __device__ void secular_root_warp(const double* __restrict__ d, const double* __restrict__ z, int K, double zz,
-                                  int i, int lane, double* omega, int* anc_out, double* mu_out, int* err) {
+                                  int i, int lane, double* omega, int* anc_out, double* mu_out, int* err,
+                                  int max_iter = 100) {
   if (K == 1) {
     if (lane == 0) {
       omega[0] = sqrt(zz);
@@ -738,7 +739,7 @@ __device__ void secular_root_warp(const double* __restrict__ d, const double* __
   double mu = 0.5 * (lo + hi);
   const double ftol = 8.0 * K * DC_EPS;
   bool done = false;
-  for (int it = 0; it < 100; ++it) {
+  for (int it = 0; it < max_iter; ++it) {  // bdc.py:589, budget max_iterations (100)
     double psi = 0.0, phi = 0.0, sa = 0.0, dpsi = 0.0, dphi = 0.0;
     for (int j = lane; j < K; j += 32) {
       const double dj = d[j], zj = z[j];
@@ -798,11 +799,12 @@ __global__ void __launch_bounds__(32 * kSecWarps) bdc_secular_kernel(const Merge
 // Standalone secular solve (solve_all_roots, bdc.py:515-525); zz from device.
 __global__ void __launch_bounds__(32 * kSecWarps) secular_standalone_kernel(const double* d, const double* z, int K,
                                                                             const double* zzp, double* omega,
-                                                                            int* anc, double* mu, int* err) {
+                                                                            int* anc, double* mu, int* err,
+                                                                            int max_iter) {
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * kSecWarps + (threadIdx.x >> 5);
   if (i >= K) return;
-  secular_root_warp(d, z, K, *zzp, i, lane, omega, anc, mu, err);
+  secular_root_warp(d, z, K, *zzp, i, lane, omega, anc, mu, err, max_iter);
 }
 
 __global__ void sumsq_kernel(const double* z, int K, double* out) {
@@ -1451,14 +1453,15 @@ __global__ void __launch_bounds__(32 * kSecWarps) secvec_standalone_kernel(const
 }
 
 int secular_run(dcsvd_ctx* h, cudaStream_t st, int K, const double* d, const double* z, double* omega, int* anc,
-                double* mu) {
+                double* mu, int max_iter) {
   if (K < 1) return set_error(h, DCSVD_EINVAL, "secular system must be nonempty");
+  if (max_iter < 0) return set_error(h, DCSVD_EINVAL, "max_iterations must be >= 0, got %d", max_iter);
   int rc = pool_reserve(h, 0, pool_bytes(1, 8), st);
   if (rc) return rc;
   double* zz = pool_take<double>(h, 0, 1);
   sumsq_kernel<<<1, 256, 0, st>>>(z, K, zz);
   secular_standalone_kernel<<<(K + kSecWarps - 1) / kSecWarps, 32 * kSecWarps, 0, st>>>(d, z, K, zz, omega, anc, mu,
-                                                                                        h->d_err);
+                                                                                        h->d_err, max_iter);
   note_launch(2);
   DC_CUDA_TRY(cudaGetLastError());
   return 0;

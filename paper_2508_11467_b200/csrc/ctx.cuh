@@ -125,7 +125,7 @@ int accuracy_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, const 
                  const double* S, const double* U, long long ldu, const double* VT, long long ldvt,
                  const double* ref, double* out_host);
 int secular_run(dcsvd_ctx* h, cudaStream_t st, int K, const double* d, const double* z, double* omega, int* anc,
-                double* mu);
+                double* mu, int max_iter);
 int loewner_run(dcsvd_ctx* h, cudaStream_t st, int K, const double* d, const double* z, const int* anc, const double* mu,
                 double* zt);
 int secvec_run(dcsvd_ctx* h, cudaStream_t st, int K, const double* d, const int* anc, const double* mu, const double* zt,

@@ -143,8 +143,6 @@ def _sys_vectors(system):
 def solve_all_roots(system, max_iterations=100):
     """All roots of the secular system, one warp per root (bdc.py:515-641).
     Frozen-lane iteration: each root's result is independent of the others."""
-    if max_iterations != 100:
-        raise ValueError("the GPU secular solver uses the reference's fixed 100-iteration budget")
     d, z, torch_in = _sys_vectors(system)
     K = d.numel()
     h = _lib.handle()
@@ -152,7 +150,7 @@ def solve_all_roots(system, max_iterations=100):
     mu = torch.empty(K, dtype=torch.float64, device=d.device)
     anc = torch.empty(K, dtype=torch.int32, device=d.device)
     rc = _lib.load_library().dcsvd_secular_roots(h, K, _lib.ptr(d), _lib.ptr(z), _lib.ptr(om), _lib.ptr(anc),
-                                                 _lib.ptr(mu), _lib.stream_ptr())
+                                                 _lib.ptr(mu), int(max_iterations), _lib.stream_ptr())
     _lib.check(rc, h)
     anc = anc.to(torch.int64)
     if torch_in:

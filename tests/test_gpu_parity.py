@@ -1007,3 +1007,60 @@ def test_rank_k_bulk_matches_cp_async(cuda, k, tb):
     c = c0.clone()
     g.matmul_accumulate(-1.0, a_odd, False, b, tb, 1.0, c)
     assert (c - ref).abs().max().item() <= 1e-12 * k
+
+
+# ---- error paths through the device status word (bdc.py:309-312, 636-639, 669-672) ----
+
+@pytest.mark.parametrize("budget", [0, 1])
+def test_secular_budget_raises_convergence_error(cuda, budget):
+    """A secular root not converged within max_iterations -> the kernel's
+    status word -> ConvergenceError, as the reference's _secular_roots
+    (bdc.py:589, 636-639) on the same system."""
+    g = _g()
+    s = g.SecularSystem(np.array([0.0, 1.0, 2.0]), np.array([1.0, 1.0, 1.0]), np.sqrt(3.0))
+    with pytest.raises(g.ConvergenceError):
+        g.solve_all_roots(s, max_iterations=budget)
+    # the handle is usable afterwards (status word reset) and the default budget converges
+    r = g.solve_all_roots(s)
+    np.testing.assert_allclose(r.omega, [0.59518794, 1.41421356, 2.37607898], rtol=1e-8)
+    r2 = g.solve_all_roots(s, max_iterations=100)
+    assert np.array_equal(r.omega, r2.omega)
+
+
+@pytest.mark.parametrize("case", [([1, 1, 2], [1.0, 1.0, 1.64575131]), ([0, 0, 2], [0.35424869, 0.35424869, 1.64575131]),
+                                  ([0, 1, 2], [0.35424869, -0.5, 1.64575131])])
+def test_loewner_nonpositive_radicand_raises_arithmetic_error(cuda, case):
+    """Roots that violate interlacing give a non-positive radicand in the
+    Loewner z update -> ArithmeticError (bdc.py:669-672); the same inputs
+    raise in the oracle (and in the reference, checked when the cases were
+    chosen)."""
+    g = _g()
+    d = np.array([0.0, 1.0, 2.0])
+    z = np.array([1.0, 1.0, 1.0])
+    anc, mu = np.array(case[0], dtype=np.intp), np.array(case[1])
+    s = g.SecularSystem(d, z, np.sqrt(3.0))
+    bad = g.SecularRoots(np.sqrt(d[anc] ** 2 + mu), anc, mu)
+    with pytest.raises(ArithmeticError):
+        oracle.loewner_z(d, z, anc, mu)
+    with pytest.raises(ArithmeticError):
+        g.recompute_z(s, bad)
+    good = g.solve_all_roots(s)
+    zt = g.recompute_z(s, good)
+    np.testing.assert_allclose(zt, oracle.loewner_z(d, z, good.anchor, good.mu), rtol=1e-13)
+
+
+def test_secular_vectors_match_oracle(cuda):
+    """secular_vectors (bdc.py:676-694) against oracle.secular_vecs on a
+    random system (round 1 checked only orthonormality)."""
+    g = _g()
+    rng = np.random.default_rng(77)
+    n = 40
+    d = np.concatenate([[0.0], np.sort(rng.uniform(0.1, 3.0, n - 1))])
+    z = rng.standard_normal(n)
+    s = g.SecularSystem(d, z, float(np.linalg.norm(z)))
+    roots = g.solve_all_roots(s)
+    zt = g.recompute_z(s, roots)
+    u, v = g.secular_vectors(s, roots, zt)
+    ou, ov = oracle.secular_vecs(d, roots.anchor, roots.mu, oracle.loewner_z(d, z, roots.anchor, roots.mu))
+    np.testing.assert_allclose(np.asarray(u), ou, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(np.asarray(v), ov, rtol=0, atol=1e-12)
