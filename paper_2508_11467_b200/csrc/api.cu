@@ -29,6 +29,7 @@ int set_rankk_min(long long mn);
 extern bool g_labrd_last_two_phase;
 extern int g_gemm_route;
 extern int g_rankk_ws;
+extern int g_dgemm_ws;
 int g_ts_literal = 1;  // TS recombination: 1 = ORGQR + GEMM (driver.py:141-142), 0 = fused reflector apply
 int set_ws_flags(int f);
 thread_local dcsvd_ctx* t_cur = nullptr;
@@ -409,6 +410,24 @@ int dcsvd_debug_ts_literal(int on) {
   return 0;
 }
 int dcsvd_debug_ws_flags(int f) { return dc::set_ws_flags(f); }
+// debug: grouped stack GEMM on host-built descriptors (copied to the device here)
+int dcsvd_debug_gemm_stack(dcsvd_handle h, const void* descs, int ndesc, int max_m, int max_n, const double* base,
+                           int64_t ld, int nbuf, void* stream) {
+  Guard g(h);
+  if (!h) return DCSVD_EINVAL;
+  dc::GemmDesc* dd = nullptr;
+  DC_CUDA_TRY(cudaMalloc(&dd, sizeof(dc::GemmDesc) * ndesc));
+  DC_CUDA_TRY(cudaMemcpy(dd, descs, sizeof(dc::GemmDesc) * ndesc, cudaMemcpyHostToDevice));
+  int rc = dc::gemm_launch_device_stack(S(stream), dd, ndesc, max_m, max_n, base, ld, nbuf);
+  cudaError_t e = cudaStreamSynchronize(S(stream));
+  cudaFree(dd);
+  if (rc) return rc;
+  return e == cudaSuccess ? 0 : dc_cuda_fail(e, "gemm_stack");
+}
+int dcsvd_debug_dgemm_ws(int on) {
+  dc::g_dgemm_ws = on;
+  return 0;
+}
 int dcsvd_debug_rankk_ws(int on) {
   dc::g_rankk_ws = on;
   return 0;

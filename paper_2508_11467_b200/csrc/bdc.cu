@@ -1356,7 +1356,10 @@ int bdsdc_run(dcsvd_ctx* h, cudaStream_t st, long long n_, const double* d, cons
                                                             h->stats_on ? h->d_flops : nullptr);
       note_launch();
       const int sidx = stat_begin(h, 2, 0.0, st);  // flops arrive through h->d_flops
-      rc = gemm_launch_device(st, false, false, gd, 4 * nm, maxn, maxn);
+      // TMA GEMM over the workspace stack W, Q, Us, Vs, S3, S4 when they are carved
+      // back to back (ld^2 doubles a multiple of the 256-byte pool granule)
+      rc = (Q == W + mat && S4 == W + 5 * mat) ? gemm_launch_device_stack(st, gd, 4 * nm, maxn, maxn, W, ld, 6) : -1;
+      if (rc < 0) rc = gemm_launch_device(st, false, false, gd, 4 * nm, maxn, maxn);
       stat_end(h, sidx, st);
       if (rc) return rc;
       const int sc = stat_begin(h, 3, 0.0, st);  // bytes arrive through h->d_flops[1]

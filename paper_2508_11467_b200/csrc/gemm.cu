@@ -3,6 +3,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <unordered_map>
 #include <vector>
 
@@ -581,13 +582,25 @@ __global__ void __launch_bounds__(256, 1) rankk_stream_kernel(GemmDesc P, int ch
 // (per-column 1-D bulk copies from one warp were issue-bound: 13 TF/s).
 int rankk_chunk(int m, int strips, int tiles, int mt, int kmax, int cmax, int sms);
 __constant__ int g_ws_flags = 0;  // debug: bit 0 = no C prefetch
-int set_ws_flags(int f) { return cudaMemcpyToSymbol(g_ws_flags, &f, sizeof(int)) == cudaSuccess ? 0 : -1; }
+int g_ws_flags_host = 0;
+int set_ws_flags(int f) {
+  g_ws_flags_host = f;
+  return cudaMemcpyToSymbol(g_ws_flags, &f, sizeof(int)) == cudaSuccess ? 0 : -1;
+}
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
   unsigned d = (unsigned)__cvta_generic_to_shared(dst), b = (unsigned)__cvta_generic_to_shared(bar);
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
       ::"r"(d), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(b) : "memory");
+}
+// TMA gather4 (sm_100): four rows (outer coordinates c[0..3]) of a box {inner, 1}
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, int x, const int (&c)[4], uint64_t* bar) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst), b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4, %5, %6}], [%7];\n" ::"r"(d), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(c[0]), "r"(c[1]), "r"(c[2]),
+      "r"(c[3]), "r"(b) : "memory");
 }
 __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n"
@@ -873,6 +886,366 @@ static int launch_rankk_ws(cudaStream_t st, const GemmDesc& d, int sms, int kmax
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialized general DMMA GEMM (host descriptor, optional split-K over
+// blockIdx.z): C = alpha op(A) op(B) + beta C on 128 x 64 tiles.  One producer
+// lane streams BK = 32 k-slices of op(A) and op(B) into an S-stage ring with
+// ONE TMA tensor-map load per operand per stage (boxes 4 elements wider than
+// the tile along the contiguous dimension: conflict-free fragment pitch; the
+// TMA unit zero-fills past K); 8 consumer warps (2 per SM sub-partition, 32 x
+// 32 each) run LDS + DMMA only and release each stage on its "empty"
+// mbarrier.  Used for the CWY inner products Z = Y^T C / C Y (K = the
+// reflector rows), X = T Z, the TS recombination U = Q U0 and other
+// long-K GEMMs.
+template <bool TA, bool TB, int S>
+struct DgemmWsCfg {
+  static constexpr int BM = 128, BN = 64, BK = 32;
+  static constexpr int WARPS_M = 4, WARPS_N = 2;
+  static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
+  static constexpr int FM = WTM / 8, FN = WTN / 8;
+  // op(A) stage: !TA [k][m] pitch BM+4 (box {BM+4, BK});  TA [m][k] pitch BK+4 (box {BK+4, BM})
+  static constexpr int LDA_S = TA ? (BK + 4) : (BM + 4);
+  static constexpr int A_ELEMS = TA ? BM * LDA_S : BK * LDA_S;
+  // op(B) stage: TB [k][n] pitch BN+4 (box {BN+4, BK});  !TB [n][k] pitch BK+4 (box {BK+4, BN})
+  static constexpr int LDB_S = TB ? (BN + 4) : (BK + 4);
+  static constexpr int B_ELEMS = TB ? BK * LDB_S : BN * LDB_S;
+  static constexpr int STAGE = A_ELEMS + B_ELEMS;
+  static constexpr int THREADS = 32 + 256;
+  static constexpr int SMEM_BYTES = S * STAGE * 8 + 128;
+};
+
+template <bool TA, bool TB, int S>
+__global__ void __launch_bounds__(288, 1)
+    dgemm_ws_kernel(GemmDesc P, int ksplit, int kchunk, long long cslice, const __grid_constant__ CUtensorMap tA,
+                    const __grid_constant__ CUtensorMap tB) {
+  using Cfg = DgemmWsCfg<TA, TB, S>;
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* sm = reinterpret_cast<double*>(smem_raw + ((128u - ((unsigned)__cvta_generic_to_shared(smem_raw) & 127u)) & 127u));
+  __shared__ __align__(8) uint64_t full[S], empty[S];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int sl = blockIdx.z;
+  const int kbeg = ksplit > 1 ? sl * kchunk : 0;
+  const int kend = ksplit > 1 ? min(P.k, kbeg + kchunk) : P.k;
+  const int KT = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tB)) : "memory");
+      const unsigned bytes = (unsigned)Cfg::STAGE * 8u;
+      for (int kt = 0; kt < KT; ++kt) {
+        const int st = kt % S;
+        if (kt >= S) mbar_wait(&empty[st], ((kt / S) - 1) & 1u);
+        double* as = sm + st * Cfg::STAGE;
+        double* bs = as + Cfg::A_ELEMS;
+        const int k0 = kbeg + kt * BK;
+        mbar_expect_tx(&full[st], bytes);
+        if (TA) tma_load_2d(as, &tA, k0, m0, &full[st]);
+        else tma_load_2d(as, &tA, m0, k0, &full[st]);
+        if (TB) tma_load_2d(bs, &tB, n0, k0, &full[st]);
+        else tma_load_2d(bs, &tB, k0, n0, &full[st]);
+      }
+    }
+    return;
+  }
+  const int cw = warp - 1;
+  const int wm = cw % Cfg::WARPS_M, wn = cw / Cfg::WARPS_M;
+  const int lr = lane >> 2, lc = lane & 3;
+  double acc[Cfg::FM][Cfg::FN][2];
+#pragma unroll
+  for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int kt = 0; kt < KT; ++kt) {
+    const int st = kt % S;
+    mbar_wait(&full[st], (kt / S) & 1u);
+    const double* as = sm + st * Cfg::STAGE;
+    const double* bs = as + Cfg::A_ELEMS;
+    // slice ends are multiples of 4 (split-K chunks of 16); past K the TMA zero-fills
+    const int kl = min(BK, ((kend - (kbeg + kt * BK)) + 3) & ~3);
+    if (kl == BK) {
+#pragma unroll
+      for (int ks = 0; ks < BK; ks += 4) {
+        double af[Cfg::FM], bf[Cfg::FN];
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i) {
+          const int m = wm * Cfg::WTM + i * 8 + lr;
+          af[i] = TA ? as[m * Cfg::LDA_S + ks + lc] : as[(ks + lc) * Cfg::LDA_S + m];
+        }
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) {
+          const int n = wn * Cfg::WTN + j * 8 + lr;
+          bf[j] = TB ? bs[(ks + lc) * Cfg::LDB_S + n] : bs[n * Cfg::LDB_S + ks + lc];
+        }
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < Cfg::FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+    } else {
+      for (int ks = 0; ks < kl; ks += 4) {
+        double af[Cfg::FM], bf[Cfg::FN];
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i) {
+          const int m = wm * Cfg::WTM + i * 8 + lr;
+          af[i] = TA ? as[m * Cfg::LDA_S + ks + lc] : as[(ks + lc) * Cfg::LDA_S + m];
+        }
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) {
+          const int n = wn * Cfg::WTN + j * 8 + lr;
+          bf[j] = TB ? bs[(ks + lc) * Cfg::LDB_S + n] : bs[n * Cfg::LDB_S + ks + lc];
+        }
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < Cfg::FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+  double* __restrict__ C = P.C + (ksplit > 1 ? sl * cslice : 0);
+  const long long ldc = P.ldc;
+  const double alpha = P.alpha, beta = P.beta;
+  const int M = P.m, N = P.n;
+#pragma unroll
+  for (int j = 0; j < Cfg::FN; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int gn = n0 + wn * Cfg::WTN + j * 8 + lc * 2 + h;
+      if (gn >= N) continue;
+      double* cc = C + (long long)gn * ldc;
+      double cv[Cfg::FM];
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i) {
+        const int gm = m0 + wm * Cfg::WTM + i * 8 + lr;
+        cv[i] = (beta != 0.0 && gm < M) ? cc[gm] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i) {
+        const int gm = m0 + wm * Cfg::WTM + i * 8 + lr;
+        if (gm < M) cc[gm] = beta != 0.0 ? fma(beta, cv[i], alpha * acc[i][j][h]) : alpha * acc[i][j][h];
+      }
+    }
+}
+
+int g_dgemm_ws = 1;  // debug: 0 = cp.async dgemm_kernel only
+
+template <bool TA, bool TB>
+static int launch_dgemm_ws(cudaStream_t st, const GemmDesc& d, int ksplit, int kchunk, long long cslice) {
+  constexpr int S = 4;
+  using Cfg = DgemmWsCfg<TA, TB, S>;
+  CUtensorMap tA, tB;
+  // op(A): !TA -> A is m x k (m contiguous); TA -> A is k x m (k contiguous)
+  if (TA) {
+    if (make_tmap_2d(&tA, d.A, d.k, d.m, d.lda, Cfg::LDA_S, Cfg::BM)) return -1;
+  } else if (make_tmap_2d(&tA, d.A, d.m, d.k, d.lda, Cfg::LDA_S, Cfg::BK)) {
+    return -1;
+  }
+  if (TB) {
+    if (make_tmap_2d(&tB, d.B, d.n, d.k, d.ldb, Cfg::LDB_S, Cfg::BK)) return -1;
+  } else if (make_tmap_2d(&tB, d.B, d.k, d.n, d.ldb, Cfg::LDB_S, Cfg::BN)) {
+    return -1;
+  }
+  auto kern = dgemm_ws_kernel<TA, TB, S>;
+  DC_CUDA_TRY((cudaError_t)func_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+  dim3 grid((d.m + Cfg::BM - 1) / Cfg::BM, (d.n + Cfg::BN - 1) / Cfg::BN, std::max(1, ksplit));
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(d, ksplit, kchunk, cslice, tA, tB);
+  note_launch();
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// Route a single host descriptor (optionally split over K) to the TMA GEMM when
+// its operands allow tensor maps and it is big enough; -1 = not taken.
+static int try_dgemm_ws(cudaStream_t st, bool ta, bool tb, const GemmBatch* b) {
+  if (!g_dgemm_ws || !b || b->count != 1) return -1;
+  const GemmDesc& d = b->d[0];
+  if (d.acol || d.ccol || d.m <= 0 || d.n <= 0 || d.k < 64) return -1;
+  if ((reinterpret_cast<uintptr_t>(d.A) & 15) || (reinterpret_cast<uintptr_t>(d.B) & 15) || (d.lda & 1) ||
+      (d.ldb & 1))
+    return -1;
+  const int ks = std::max(1, b->ksplit);
+  if (ks > 1 && (b->kchunk & 3)) return -1;
+  const long long tiles = (long long)((d.m + 127) / 128) * ((d.n + 63) / 64) * ks;
+  if (tiles < 148) return -1;  // too few tiles for one CTA per SM
+  if (!ta && !tb) return launch_dgemm_ws<false, false>(st, d, ks, b->kchunk, b->cslice);
+  if (!ta && tb) return launch_dgemm_ws<false, true>(st, d, ks, b->kchunk, b->cslice);
+  if (ta && !tb) return launch_dgemm_ws<true, false>(st, d, ks, b->kchunk, b->cslice);
+  return launch_dgemm_ws<true, true>(st, d, ks, b->kchunk, b->cslice);
+}
+
+// ---------------------------------------------------------------------------
+// The BDC merge products (bdc.py:701-747) on the TMA GEMM: device descriptors
+// (one per blockIdx.z) whose A columns are gathered through `acol` and whose C
+// columns are scattered through `ccol`.  All operands live in one stack of
+// equally shaped ld x ld workspaces (W, Q, Us, Vs, S3, S4 carved back to back),
+// so ONE pair of tensor maps over that stack serves every descriptor: op(A)
+// stage column kk is one TMA box {BM + 4, 1} at (row0 + m0, stack column of
+// acol[k0 + kk]), issued four columns per TMA gather4 instruction (BK / 4 per
+// stage from the producer lane), and op(B) one box {BK + 4, BN}.  Past a descriptor's K the stage holds other data, so
+// the consumers zero both fragments there (NaN-safe).
+template <int S>
+__global__ void __launch_bounds__(288, 1)
+    dgemm_ws_gather_kernel(const GemmDesc* __restrict__ ddesc, const double* base, long long ld,
+                           const __grid_constant__ CUtensorMap tAg, const __grid_constant__ CUtensorMap tB) {
+  using Cfg = DgemmWsCfg<false, false, S>;
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK;
+  const GemmDesc P = ddesc[blockIdx.z];
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  if (m0 >= P.m || n0 >= P.n) return;
+  if (P.k <= 0) {  // empty class block: the product is zero (beta = 0 overwrites)
+    for (int idx = threadIdx.x; idx < BM * BN; idx += blockDim.x) {
+      const int i = m0 + idx % BM, j = n0 + idx / BM;
+      if (i < P.m && j < P.n) P.C[i + (long long)(P.ccol ? P.ccol[j] : j) * P.ldc] = 0.0;
+    }
+    return;
+  }
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* sm = reinterpret_cast<double*>(smem_raw + ((128u - ((unsigned)__cvta_generic_to_shared(smem_raw) & 127u)) & 127u));
+  __shared__ __align__(8) uint64_t full[S], empty[S];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int K = P.k;
+  const int KT = (K + BK - 1) / BK;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0) {
+      const long long offA = P.A - base, offB = P.B - base;
+      const int rowA = (int)(offA % ld), colA = (int)(offA / ld);
+      const int rowB = (int)(offB % ld), colB = (int)(offB / ld);
+      const int* __restrict__ acol = P.acol;
+      for (int kt = 0; kt < KT; ++kt) {
+        const int st = kt % S;
+        if (kt >= S) mbar_wait(&empty[st], ((kt / S) - 1) & 1u);
+        double* as = sm + st * Cfg::STAGE;
+        double* bs = as + Cfg::A_ELEMS;
+        const int k0 = kt * BK;
+        const int nk = min(BK, K - k0);
+        const int ng = (nk + 3) >> 2;  // gather4 groups (a group's dst is 4 x 1056 B: 128-byte aligned)
+        mbar_expect_tx(&full[st], (unsigned)(4 * ng * Cfg::LDA_S + Cfg::B_ELEMS) * 8u);
+        for (int q = 0; q < ng; ++q) {
+          int c[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) c[i] = colA + acol[k0 + min(4 * q + i, nk - 1)];  // tail: repeat (masked)
+          // the box's inner start must be 16-byte aligned: odd rows start one row early
+          tma_gather4(as + 4 * q * Cfg::LDA_S, &tAg, (rowA & ~1) + m0, c, &full[st]);
+        }
+        tma_load_2d(bs, &tB, (rowB & ~1) + k0, colB + n0, &full[st]);
+      }
+    }
+    return;
+  }
+  const int cw = warp - 1;
+  const int wm = cw % Cfg::WARPS_M, wn = cw / Cfg::WARPS_M;
+  const int lr = lane >> 2, lc = lane & 3;
+  // odd operand row offsets were loaded one row early (16-byte aligned box starts)
+  const int shA = (int)((P.A - base) % ld) & 1, shB = (int)((P.B - base) % ld) & 1;
+  double acc[Cfg::FM][Cfg::FN][2];
+#pragma unroll
+  for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int kt = 0; kt < KT; ++kt) {
+    const int st = kt % S;
+    mbar_wait(&full[st], (kt / S) & 1u);
+    const double* as = sm + st * Cfg::STAGE + shA;
+    const double* bs = sm + st * Cfg::STAGE + Cfg::A_ELEMS + shB;
+    const int kl = K - kt * BK;  // valid k of this stage (>= BK: full)
+    if (kl >= BK) {
+#pragma unroll
+      for (int ks = 0; ks < BK; ks += 4) {
+        double af[Cfg::FM], bf[Cfg::FN];
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i) af[i] = as[(ks + lc) * Cfg::LDA_S + wm * Cfg::WTM + i * 8 + lr];
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) bf[j] = bs[(wn * Cfg::WTN + j * 8 + lr) * Cfg::LDB_S + ks + lc];
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < Cfg::FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+    } else {
+      for (int ks = 0; ks < kl; ks += 4) {
+        const bool ok = ks + lc < kl;
+        double af[Cfg::FM], bf[Cfg::FN];
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i) af[i] = ok ? as[(ks + lc) * Cfg::LDA_S + wm * Cfg::WTM + i * 8 + lr] : 0.0;
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) bf[j] = ok ? bs[(wn * Cfg::WTN + j * 8 + lr) * Cfg::LDB_S + ks + lc] : 0.0;
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < Cfg::FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+  double* __restrict__ C = P.C;
+  const long long ldc = P.ldc;
+  const int* __restrict__ ccol = P.ccol;
+  const double alpha = P.alpha;
+  const int M = P.m, N = P.n;
+#pragma unroll
+  for (int j = 0; j < Cfg::FN; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int gn = n0 + wn * Cfg::WTN + j * 8 + lc * 2 + h;
+      if (gn >= N) continue;
+      double* cc = C + (long long)(ccol ? ccol[gn] : gn) * ldc;
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i) {
+        const int gm = m0 + wm * Cfg::WTM + i * 8 + lr;
+        if (gm < M) cc[gm] = alpha * acc[i][j][h];  // beta = 0 (merge products overwrite)
+      }
+    }
+}
+
+// Grouped merge products on the TMA GEMM when the workspaces form one stack
+// (`base`, `nbuf` ld x ld buffers back to back, 16-byte aligned, ld even);
+// -1 = not taken (caller falls back to dgemm_kernel with gather).
+int gemm_launch_device_stack(cudaStream_t st, const GemmDesc* ddesc, int ndesc, int max_m, int max_n,
+                             const double* base, long long ld, int nbuf) {
+  if (!g_dgemm_ws || (ld & 1) || (reinterpret_cast<uintptr_t>(base) & 15) || ld * nbuf > (1LL << 31)) {
+    if (g_ws_flags_host & 8) fprintf(stderr, "stack: precondition %d %lld %p\n", g_dgemm_ws, ld, (const void*)base);
+    return -1;
+  }
+  constexpr int S = 4;
+  using Cfg = DgemmWsCfg<false, false, S>;
+  CUtensorMap tAg, tB;
+  if (make_tmap_2d(&tAg, base, ld, ld * nbuf, ld, Cfg::LDA_S, 1)) {
+    if (g_ws_flags_host & 8) fprintf(stderr, "stack: tAg encode failed\n");
+    return -1;
+  }
+  if (make_tmap_2d(&tB, base, ld, ld * nbuf, ld, Cfg::LDB_S, Cfg::BN)) {
+    if (g_ws_flags_host & 8) fprintf(stderr, "stack: tB encode failed\n");
+    return -1;
+  }
+  auto kern = dgemm_ws_gather_kernel<S>;
+  DC_CUDA_TRY((cudaError_t)func_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+  dim3 grid((max_m + Cfg::BM - 1) / Cfg::BM, (max_n + Cfg::BN - 1) / Cfg::BN, ndesc);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(ddesc, base, ld, tAg, tB);
+  note_launch();
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 // Row tiles per work unit.  The CTAs take units round-robin, so the kernel's
 // time is the largest per-CTA sum of unit costs: the unit's rows in tiles
 // (the last tile may be short) plus a fixed start cost `s` for loading its B
@@ -1007,7 +1380,8 @@ int gemm_launch(cudaStream_t st, bool ta, bool tb, const GemmDesc& d) {
     GemmBatch b;
     b.d[0] = d;
     b.count = 1;
-    r = dispatch(st, ta, tb, &b, nullptr, 1, d.m, d.n, d.k, d.beta != 0.0);
+    r = try_dgemm_ws(st, ta, tb, &b);
+    if (r < 0) r = dispatch(st, ta, tb, &b, nullptr, 1, d.m, d.n, d.k, d.beta != 0.0);
   }
   if (t_cur) stat_end(t_cur, sidx, st);
   return r;
@@ -1025,8 +1399,9 @@ int gemm_launch_batch(cudaStream_t st, bool ta, bool tb, const GemmBatch& b) {
     flops += 2.0 * b.d[i].m * b.d[i].n * b.d[i].k;
   }
   const int sidx = t_cur ? stat_begin(t_cur, 1, flops, st) : -1;
-  const int r = dispatch(st, ta, tb, &b, nullptr, b.count * std::max(1, b.ksplit), mm, nn,
-                         b.ksplit > 1 ? b.kchunk : kk, bnz);
+  int r = try_dgemm_ws(st, ta, tb, &b);
+  if (r < 0)
+    r = dispatch(st, ta, tb, &b, nullptr, b.count * std::max(1, b.ksplit), mm, nn, b.ksplit > 1 ? b.kchunk : kk, bnz);
   if (t_cur) stat_end(t_cur, sidx, st);
   return r;
 }

@@ -46,6 +46,11 @@ int gemm_launch(cudaStream_t st, bool ta, bool tb, const GemmDesc& d);
 int gemm_launch_batch(cudaStream_t st, bool ta, bool tb, const GemmBatch& b);
 // Grouped: `ndesc` descriptors in device memory (built by device code); the
 // grid covers max_m x max_n tiles per descriptor, extra CTAs exit.
+// Same for descriptors whose operands all live in one stack of `nbuf` equally
+// shaped ld x ld buffers starting at `base` (TMA GEMM, beta = 0, no transposes);
+// returns -1 when not applicable.
+int gemm_launch_device_stack(cudaStream_t st, const GemmDesc* ddesc, int ndesc, int max_m, int max_n,
+                             const double* base, long long ld, int nbuf);
 int gemm_launch_device(cudaStream_t st, bool ta, bool tb, const GemmDesc* ddesc, int ndesc,
                        int max_m, int max_n);
 

@@ -1064,3 +1064,52 @@ def test_secular_vectors_match_oracle(cuda):
     ou, ov = oracle.secular_vecs(d, roots.anchor, roots.mu, oracle.loewner_z(d, z, roots.anchor, roots.mu))
     np.testing.assert_allclose(np.asarray(u), ou, rtol=0, atol=1e-12)
     np.testing.assert_allclose(np.asarray(v), ov, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("ta", [False, True])
+@pytest.mark.parametrize("tb", [False, True])
+@pytest.mark.parametrize("shape", [(1000, 2000, 300), (1537, 1029, 97), (128, 9000, 4000)])
+def test_tma_gemm_matches_torch(cuda, ta, tb, shape):
+    """General GEMMs large enough for the warp-specialized TMA kernel
+    (dgemm_ws_kernel: >= 148 output tiles, 16-byte-aligned operands), every
+    transpose combination, K not a multiple of the 32-wide stage (TMA zero
+    fill), beta != 0; against torch fp64, and against the cp.async kernel."""
+    g = _g()
+    lib = _lib_handle()
+    m, n, k = shape
+    torch.manual_seed(m + n + k)
+    a = torch.randn(k, m, dtype=torch.float64, device=cuda).t() if not ta else torch.randn(m, k, dtype=torch.float64, device=cuda).t()
+    b = torch.randn(n, k, dtype=torch.float64, device=cuda).t() if not tb else torch.randn(k, n, dtype=torch.float64, device=cuda).t()
+    c0 = torch.randn(n, m, dtype=torch.float64, device=cuda).t()
+    ref = 0.5 * c0 + 1.25 * ((a.t() if ta else a) @ (b.t() if tb else b))
+    outs = []
+    for ws in (1, 0):
+        lib.dcsvd_debug_dgemm_ws(ws)
+        try:
+            c = c0.clone()
+            g.matmul_accumulate(1.25, a, ta, b, tb, 0.5, c)
+        finally:
+            lib.dcsvd_debug_dgemm_ws(1)
+        assert (c - ref).abs().max().item() <= 1e-12 * k * ref.abs().max().item()
+        outs.append(c)
+    assert (outs[0] - outs[1]).abs().max().item() <= 1e-13 * k * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("n", [1000, 2048])
+def test_bdc_merge_products_tma_vs_cpasync(cuda, n):
+    """BDC merge products on the TMA gather GEMM (workspace stack, gather4
+    A columns, odd row offsets loaded one row early) are bitwise equal to the
+    cp.async gather kernel's (same k order per output)."""
+    g = _g()
+    lib = _lib_handle()
+    a = g.generate_matrix(g.MatrixSpec("random", n, n, seed=9), device=True)
+    f = g.gebrd_blocked(a)
+    prob = g.BidiagonalProblem(f.d, f.e)
+    r1 = g.bdsdc(prob)
+    lib.dcsvd_debug_dgemm_ws(0)
+    try:
+        r0 = g.bdsdc(prob)
+    finally:
+        lib.dcsvd_debug_dgemm_ws(1)
+    assert torch.equal(r0.dvals, r1.dvals)
+    assert torch.equal(r0.w, r1.w) and torch.equal(r0.qfull, r1.qfull)
