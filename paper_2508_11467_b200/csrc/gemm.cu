@@ -1040,6 +1040,148 @@ __global__ void __launch_bounds__(288, 1)
 
 int g_dgemm_ws = 1;  // debug: 0 = cp.async dgemm_kernel only
 
+// Persistent rank-k update on the TMA GEMM tiles (C <- C -+ A op(B), K <= 128,
+// beta = 1, alpha = +-1): 128 x 64 output tiles taken round-robin; the
+// producer lane streams every tile's BK = 32 k-slices of A and op(B) through
+// the S-stage ring without stopping between tiles, so the next tile's first
+// stages are resident when its math starts; the 8 consumer warps hold the
+// current tile's accumulators (initialised from C, the sign of alpha applied
+// by integer XOR) and the NEXT tile's C fragment (loaded at the start of the
+// current tile's math), so the per-tile epilogue is plain stores.
+template <bool TB, int S>
+__global__ void __launch_bounds__(288, 1)
+    rankk_tile_kernel(GemmDesc P, const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB) {
+  using Cfg = DgemmWsCfg<false, TB, S>;
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* sm = reinterpret_cast<double*>(smem_raw + ((128u - ((unsigned)__cvta_generic_to_shared(smem_raw) & 127u)) & 127u));
+  __shared__ __align__(8) uint64_t full[S], empty[S];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int M = P.m, N = P.n, K = P.k;
+  const int tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN, ntiles = tm * tn;
+  const int KT = (K + BK - 1) / BK;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tB)) : "memory");
+      const unsigned bytes = (unsigned)Cfg::STAGE * 8u;
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int m0 = (t % tm) * BM, n0 = (t / tm) * BN;
+        for (int kt = 0; kt < KT; ++kt, ++it) {
+          const int st = it % S;
+          if (it >= S) mbar_wait(&empty[st], ((it / S) - 1) & 1u);
+          double* as = sm + st * Cfg::STAGE;
+          double* bs = as + Cfg::A_ELEMS;
+          mbar_expect_tx(&full[st], bytes);
+          tma_load_2d(as, &tA, m0, kt * BK, &full[st]);
+          if (TB) tma_load_2d(bs, &tB, n0, kt * BK, &full[st]);
+          else tma_load_2d(bs, &tB, kt * BK, n0, &full[st]);
+        }
+      }
+    }
+    return;
+  }
+  const int cw = warp - 1;
+  const int wm = cw % Cfg::WARPS_M, wn = cw / Cfg::WARPS_M;
+  const int lr = lane >> 2, lc = lane & 3;
+  double* __restrict__ C = P.C;
+  const long long ldc = P.ldc;
+  const bool negb = P.alpha == -1.0;
+  auto load_c = [&](int t, double (&dst)[Cfg::FM][Cfg::FN][2]) {
+    const int m0 = (t % tm) * BM, n0 = (t / tm) * BN;
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gn = n0 + wn * Cfg::WTN + j * 8 + lc * 2 + h;
+        const double* cc = C + (long long)gn * ldc + m0 + wm * Cfg::WTM + lr;
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i)
+          dst[i][j][h] = (gn < N && m0 + wm * Cfg::WTM + i * 8 + lr < M) ? __ldcg(cc + i * 8) : 0.0;
+      }
+  };
+  double cn[Cfg::FM][Cfg::FN][2];
+  if ((int)blockIdx.x < ntiles) load_c(blockIdx.x, cn);
+  int it = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int m0 = (t % tm) * BM, n0 = (t / tm) * BN;
+    double acc[Cfg::FM][Cfg::FN][2];
+    // C -= A op(B) runs as -((-C) + A op(B)): sign flips by integer XOR on the load / store
+#pragma unroll
+    for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) acc[i][j][h] = negb ? neg_bits(cn[i][j][h]) : cn[i][j][h];
+    if (t + (int)gridDim.x < ntiles) load_c(t + gridDim.x, cn);  // next tile's C, in flight during the math
+    for (int kt = 0; kt < KT; ++kt, ++it) {
+      const int st = it % S;
+      mbar_wait(&full[st], (it / S) & 1u);
+      const double* as = sm + st * Cfg::STAGE;
+      const double* bs = as + Cfg::A_ELEMS;
+#pragma unroll
+      for (int ks = 0; ks < BK; ks += 4) {  // past K the TMA zero-filled both operands
+        double af[Cfg::FM], bf[Cfg::FN];
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i) af[i] = as[(ks + lc) * Cfg::LDA_S + wm * Cfg::WTM + i * 8 + lr];
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) {
+          const int n = wn * Cfg::WTN + j * 8 + lr;
+          bf[j] = TB ? bs[(ks + lc) * Cfg::LDB_S + n] : bs[n * Cfg::LDB_S + ks + lc];
+        }
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < Cfg::FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gn = n0 + wn * Cfg::WTN + j * 8 + lc * 2 + h;
+        double* cc = C + (long long)gn * ldc + m0 + wm * Cfg::WTM + lr;
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i)
+          if (gn < N && m0 + wm * Cfg::WTM + i * 8 + lr < M) cc[i * 8] = negb ? neg_bits(acc[i][j][h]) : acc[i][j][h];
+      }
+  }
+}
+
+template <bool TB>
+static int launch_rankk_tile(cudaStream_t st, const GemmDesc& d, int sms) {
+  constexpr int S = 4;
+  using Cfg = DgemmWsCfg<false, TB, S>;
+  CUtensorMap tA, tB;
+  if (make_tmap_2d(&tA, d.A, d.m, d.k, d.lda, Cfg::LDA_S, Cfg::BK)) return -1;
+  if (TB) {
+    if (make_tmap_2d(&tB, d.B, d.n, d.k, d.ldb, Cfg::LDB_S, Cfg::BK)) return -1;
+  } else if (make_tmap_2d(&tB, d.B, d.k, d.n, d.ldb, Cfg::LDB_S, Cfg::BN)) {
+    return -1;
+  }
+  auto kern = rankk_tile_kernel<TB, S>;
+  DC_CUDA_TRY((cudaError_t)func_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+  const long long ntiles = (long long)((d.m + Cfg::BM - 1) / Cfg::BM) * ((d.n + Cfg::BN - 1) / Cfg::BN);
+  const int grid = (int)std::max(1LL, std::min<long long>(ntiles, sms));
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(d, tA, tB);
+  note_launch();
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+
+
 template <bool TA, bool TB>
 static int launch_dgemm_ws(cudaStream_t st, const GemmDesc& d, int ksplit, int kchunk, long long cslice) {
   constexpr int S = 4;
@@ -1341,11 +1483,28 @@ static int sm_count() {
 
 // Route rank-k updates (K <= 128, M x N >= 512^2, plain strided operands) to the
 // streaming kernel.  Returns -1 when the shape does not qualify.
+static int try_dgemm_ws(cudaStream_t st, bool ta, bool tb, const GemmBatch* b);
 static int try_rankk(cudaStream_t st, bool ta, bool tb, const GemmDesc& d) {
   if (g_gemm_route != 0) return -1;
   if (ta || d.acol || d.ccol || d.k < 1 || d.k > 128 || d.beta == 0.0) return -1;
   if ((long long)d.m * d.n < g_rankk_min_mn || d.m < 256) return -1;
   const int sms = sm_count();
+  if (g_dgemm_ws == 2 && d.k > 64) {  // debug: rank-k updates on the (non-persistent) general TMA GEMM
+    GemmBatch b;
+    b.d[0] = d;
+    b.count = 1;
+    const int r = try_dgemm_ws(st, ta, tb, &b);
+    if (r >= 0) return r;
+  }
+  // K > 64 (the 128-wide CWY updates of ORMBR / GEQRF / ORGQR): persistent
+  // 128 x 64-tile TMA kernel with folded C (8192^2 K = 128: 24.7 -> 29.0
+  // TFLOP/s, C2 ORMBR 84.6 -> 79.7 ms); at K = 64 it does not beat the
+  // streaming kernel (21.0 vs 21.5), which keeps the GEBRD trailing update.
+  if (g_dgemm_ws && d.k > 64 && d.beta == 1.0 && (d.alpha == 1.0 || d.alpha == -1.0) &&
+      !((reinterpret_cast<uintptr_t>(d.A) & 15) || (reinterpret_cast<uintptr_t>(d.B) & 15) || (d.lda & 1) || (d.ldb & 1))) {
+    const int r = tb ? launch_rankk_tile<true>(st, d, sms) : launch_rankk_tile<false>(st, d, sms);
+    if (r >= 0) return r;
+  }
   // TMA tensor maps need 16-byte-aligned bases and leading dimensions.  The
   // warp-specialized kernel wins for K > 64 (8192^2 K = 128: 24.0 -> 24.9
   // TFLOP/s, C2 ORMBR 90.0 -> 87.3 ms); at K <= 64 (GEBRD trailing update)

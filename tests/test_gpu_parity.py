@@ -447,10 +447,12 @@ def test_rank_k_update_kernel(cuda, k, tb, m, ab):
     assert (c - ref).abs().max().item() <= 1e-12 * max(k, 1)
 
 
-@pytest.mark.parametrize("ws", [0, 1])
+@pytest.mark.parametrize("ws", [(1, 1), (0, 1), (0, 0)])
 def test_rank_k_kernels_agree_on_pipeline_shapes(cuda, ws):
-    """The ORMBR-shaped rank-128 update (8192 x 4096, C -= Y X) through both
-    rank-k kernels (dcsvd_debug_rankk_ws) against torch."""
+    """The ORMBR-shaped rank-128 update (8192 x 4096, C -= Y X) through the
+    persistent TMA tile kernel (default), the 3-group TMA kernel
+    (dcsvd_debug_dgemm_ws(0)) and the cp.async streaming kernel (both off),
+    against torch."""
     g = _g()
     lib = _lib_handle()
     torch.manual_seed(5)
@@ -459,10 +461,12 @@ def test_rank_k_kernels_agree_on_pipeline_shapes(cuda, ws):
     b = torch.randn(n, k, dtype=torch.float64, device=cuda).t()
     c = torch.randn(n, m, dtype=torch.float64, device=cuda).t()
     ref = c - a @ b
-    lib.dcsvd_debug_rankk_ws(ws)
+    lib.dcsvd_debug_dgemm_ws(ws[0])
+    lib.dcsvd_debug_rankk_ws(ws[1])
     try:
         g.matmul_accumulate(-1.0, a, False, b, False, 1.0, c)
     finally:
+        lib.dcsvd_debug_dgemm_ws(1)
         lib.dcsvd_debug_rankk_ws(1)
     assert (c - ref).abs().max().item() <= 1e-12 * k
 
