@@ -654,9 +654,11 @@ def main():
         "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
         "frac": (achieved / hbm) if achieved else None,
         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-        "traffic": ncu.get("labrd_dram_bytes_per_launch"),
-        "traffic_note": ("ncu --set full capture of the first C2 panel (labrd4_kernel, view 8192x8192, nb=32, "
-                         "algorithmic 3.42e10 B): DRAM bytes per launch; the L2 snake keeps it below the algorithmic bytes"),
+        "traffic": ncu.get("labrd_dram_bytes_per_step") if args.workload == "c2" else None,
+        "traffic_note": ("DRAM bytes per step = sum of dram__bytes_read + dram__bytes_write over all 241 LABRD/GEBD2 "
+                         "launches of one 8192^2 GEBRD (ncu --cache-control none, profiles/labrd_dram_r02.csv, "
+                         "profiles/ncu_r02_labrd_dram.md): 65 % of the algorithmic bytes -- the snake order and L2 "
+                         "hints serve the rest from L2") if args.workload == "c2" else "C2 capture only",
         "algorithmic_bytes_per_step": lab_bytes / max(args.steps, 1),
         "launches_per_step": lab_n / max(args.steps, 1),
         "share_of_step": (lab_ms / args.steps) / t_ms if t_ms > 0 else None,
@@ -667,8 +669,9 @@ def main():
     dmma_peak = 148 * 128 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
     gem_achieved = (gem_flops / (gem_ms * 1e-3) / 1e12) if gem_ms > 0 else None
     roof_gem = {
-        "kernel": "dgemm_kernel + rankk_stream_kernel (all DMMA GEMMs: GEBRD trailing, CWY ORMBR/GEQRF/ORGQR, "
-                  "TS recombination, BDC merge products)",
+        "kernel": "all DMMA GEMMs: dgemm_ws_kernel (TMA, long K: CWY inner products, TS U = Q U0), rankk_tile_kernel "
+                  "(TMA, CWY rank-128 updates), rankk_stream_kernel (GEBRD rank-64 trailing update), "
+                  "dgemm_ws_gather_kernel (TMA gather4, BDC merge products), dgemm_kernel (fallback)",
         "bound": "tensor", "achieved": gem_achieved, "peak": dmma_peak, "unit": "TFLOP/s",
         "frac": (gem_achieved / dmma_peak) if gem_achieved else None,
         "peak_source": "FP64 DMMA peak 148 SMs x 128 flop/clk at sm_max_mhz (MEASURED_PEAKS.json); cuBLAS DGEMM "
