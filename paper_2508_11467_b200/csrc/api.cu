@@ -30,6 +30,7 @@ extern bool g_labrd_last_two_phase;
 extern int g_gemm_route;
 extern int g_rankk_ws;
 extern int g_dgemm_ws;
+extern int g_cwy_split_mode;
 int g_ts_literal = 1;  // TS recombination: 1 = ORGQR + GEMM (driver.py:141-142), 0 = fused reflector apply
 int set_ws_flags(int f);
 thread_local dcsvd_ctx* t_cur = nullptr;
@@ -423,6 +424,10 @@ int dcsvd_debug_gemm_stack(dcsvd_handle h, const void* descs, int ndesc, int max
   cudaFree(dd);
   if (rc) return rc;
   return e == cudaSuccess ? 0 : dc_cuda_fail(e, "gemm_stack");
+}
+int dcsvd_debug_cwy_split(int mode) {
+  dc::g_cwy_split_mode = mode;
+  return 0;
 }
 int dcsvd_debug_dgemm_ws(int on) {
   dc::g_dgemm_ws = on;

@@ -1038,7 +1038,7 @@ __global__ void __launch_bounds__(288, 1)
     }
 }
 
-int g_dgemm_ws = 1;  // debug: 0 = cp.async dgemm_kernel only
+int g_dgemm_ws = 1;  // debug: 0 = cp.async dgemm_kernel only, 2 = rank-k on the non-persistent TMA GEMM, 3 = rank-k tile kernel at any K
 
 // Persistent rank-k update on the TMA GEMM tiles (C <- C -+ A op(B), K <= 128,
 // beta = 1, alpha = +-1): 128 x 64 output tiles taken round-robin; the
@@ -1500,7 +1500,7 @@ static int try_rankk(cudaStream_t st, bool ta, bool tb, const GemmDesc& d) {
   // 128 x 64-tile TMA kernel with folded C (8192^2 K = 128: 24.7 -> 29.0
   // TFLOP/s, C2 ORMBR 84.6 -> 79.7 ms); at K = 64 it does not beat the
   // streaming kernel (21.0 vs 21.5), which keeps the GEBRD trailing update.
-  if (g_dgemm_ws && d.k > 64 && d.beta == 1.0 && (d.alpha == 1.0 || d.alpha == -1.0) &&
+  if (g_dgemm_ws && (d.k > 64 || g_dgemm_ws == 3) && d.beta == 1.0 && (d.alpha == 1.0 || d.alpha == -1.0) &&
       !((reinterpret_cast<uintptr_t>(d.A) & 15) || (reinterpret_cast<uintptr_t>(d.B) & 15) || (d.lda & 1) || (d.ldb & 1))) {
     const int r = tb ? launch_rankk_tile<true>(st, d, sms) : launch_rankk_tile<false>(st, d, sms);
     if (r >= 0) return r;

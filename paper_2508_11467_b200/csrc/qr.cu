@@ -151,14 +151,35 @@ static int grid_for(long long n, int threads = 256) {
 // ~3 CTAs per SM, slices of >= 128 rows, partials <= 16M doubles.
 constexpr int kMaxKSplit = 128;  // split-K slices (in-kernel, GemmBatch::ksplit)
 
+int g_cwy_split_mode = 1;  // debug: 0 = round-1 rule (>= 2 tiles of 64 x 128 per SM)
 static int cwy_split(int sms, int w, long long c_other, long long rows_y) {
-  // count 64x128 tiles: enough of them (>= 2 per SM) selects the 2-CTA/SM DMMA config
-  const long long zt = ((w + 63) / 64) * ((c_other + 127) / 128);
-  int S = 1;
-  while (S < kMaxKSplit && zt * S < 2LL * sms && rows_y / (S * 2) >= 256 &&
-         (long long)(2 * S) * w * c_other <= (16LL << 20))
-    S *= 2;
-  return S;
+  if (g_cwy_split_mode == 0) {
+    // count 64x128 tiles: enough of them (>= 2 per SM) selects the 2-CTA/SM DMMA config
+    const long long zt = ((w + 63) / 64) * ((c_other + 127) / 128);
+    int S = 1;
+    while (S < kMaxKSplit && zt * S < 2LL * sms && rows_y / (S * 2) >= 256 &&
+           (long long)(2 * S) * w * c_other <= (16LL << 20))
+      S *= 2;
+    return S;
+  }
+  // The inner products run on the TMA GEMM (128 x 64 tiles, one CTA per SM):
+  // pick the split with the smallest wave-quantised time ceil(T S / sms) / S,
+  // plus a ~2 us pipeline fill per CTA (a full-K CTA streams ~65 ns per row of
+  // Y); K slices of >= 256 rows, partials <= 16M doubles.
+  const long long T = ((w + 127) / 128) * ((c_other + 63) / 64);
+  int best = 1;
+  double bt = 1e300;
+  for (int S = 1; S <= kMaxKSplit; ++S) {
+    if (S > 1 && rows_y / S < 256) break;
+    if (S > 1 && (long long)S * w * c_other > (16LL << 20)) break;
+    const double waves = (double)((T * S + sms - 1) / sms);
+    const double t = waves * ((double)rows_y / S * 65e-9 + 2e-6);
+    if (t < bt * 0.99) {
+      bt = t;
+      best = S;
+    }
+  }
+  return best;
 }
 
 static size_t cwy_scratch_doubles(int sms, long long rows_y, long long c_other, int w) {
