@@ -1038,7 +1038,7 @@ __global__ void __launch_bounds__(288, 1)
     }
 }
 
-int g_dgemm_ws = 1;  // debug: 0 = cp.async dgemm_kernel only, 2 = rank-k on the non-persistent TMA GEMM, 3 = rank-k tile kernel at any K
+int g_dgemm_ws = 1;  // debug: 0 = cp.async kernels only, 2 = rank-k (K > 64) on the non-persistent TMA GEMM, 3 = register-C rank-k tile kernel
 
 // Persistent rank-k update on the TMA GEMM tiles (C <- C -+ A op(B), K <= 128,
 // beta = 1, alpha = +-1): 128 x 64 output tiles taken round-robin; the
@@ -1157,6 +1157,152 @@ __global__ void __launch_bounds__(288, 1)
           if (gn < N && m0 + wm * Cfg::WTM + i * 8 + lr < M) cc[i * 8] = negb ? neg_bits(acc[i][j][h]) : acc[i][j][h];
       }
   }
+}
+
+// Variant of rankk_tile_kernel with the C tile staged in shared memory by the
+// producer (TMA box {130, 64}: pitch 130 makes the (row, 2-column) fragment
+// reads conflict-free), one tile ahead behind a c_full / c_empty pair of
+// mbarriers, so the consumers need registers for the accumulators only (no
+// next-tile C fragment: the register-resident version spills at the 168-register
+// cap of 9 warps, and its reloads stalled the K = 64 update).
+template <bool TB, int S>
+struct RankkTileCCfg {
+  using G = DgemmWsCfg<false, TB, S>;
+  static constexpr int LDC_S = 130;
+  static constexpr int C_ELEMS = LDC_S * G::BN;
+  static constexpr int SMEM_BYTES = (S * G::STAGE + C_ELEMS) * 8 + 128;
+};
+
+template <bool TB, int S>
+__global__ void __launch_bounds__(288, 1)
+    rankk_tilec_kernel(GemmDesc P, const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
+                       const __grid_constant__ CUtensorMap tC) {
+  using Cfg = DgemmWsCfg<false, TB, S>;
+  using CC = RankkTileCCfg<TB, S>;
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* sm = reinterpret_cast<double*>(smem_raw + ((128u - ((unsigned)__cvta_generic_to_shared(smem_raw) & 127u)) & 127u));
+  double* cs = sm + S * Cfg::STAGE;  // C tile [n][m], pitch 130
+  __shared__ __align__(8) uint64_t full[S], empty[S], c_full, c_empty;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int M = P.m, N = P.n, K = P.k;
+  const int tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN, ntiles = tm * tn;
+  const int KT = (K + BK - 1) / BK;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+    }
+    mbar_init(&c_full, 1);
+    mbar_init(&c_empty, 8);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tB)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tC)) : "memory");
+      const unsigned bytes = (unsigned)Cfg::STAGE * 8u;
+      int it = 0, tc = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tc) {
+        const int m0 = (t % tm) * BM, n0 = (t / tm) * BN;
+        // C of this tile once the consumers have read the previous one
+        if (tc > 0) mbar_wait(&c_empty, (tc - 1) & 1u);
+        mbar_expect_tx(&c_full, (unsigned)CC::C_ELEMS * 8u);
+        tma_load_2d(cs, &tC, m0, n0, &c_full);
+        for (int kt = 0; kt < KT; ++kt, ++it) {
+          const int st = it % S;
+          if (it >= S) mbar_wait(&empty[st], ((it / S) - 1) & 1u);
+          double* as = sm + st * Cfg::STAGE;
+          double* bs = as + Cfg::A_ELEMS;
+          mbar_expect_tx(&full[st], bytes);
+          tma_load_2d(as, &tA, m0, kt * BK, &full[st]);
+          if (TB) tma_load_2d(bs, &tB, n0, kt * BK, &full[st]);
+          else tma_load_2d(bs, &tB, kt * BK, n0, &full[st]);
+        }
+      }
+    }
+    return;
+  }
+  const int cw = warp - 1;
+  const int wm = cw % Cfg::WARPS_M, wn = cw / Cfg::WARPS_M;
+  const int lr = lane >> 2, lc = lane & 3;
+  double* __restrict__ C = P.C;
+  const long long ldc = P.ldc;
+  const bool negb = P.alpha == -1.0;
+  int it = 0, tc = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tc) {
+    const int m0 = (t % tm) * BM, n0 = (t / tm) * BN;
+    double acc[Cfg::FM][Cfg::FN][2];
+    mbar_wait(&c_full, tc & 1u);
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double* cc = cs + (wn * Cfg::WTN + j * 8 + lc * 2 + h) * CC::LDC_S + wm * Cfg::WTM + lr;
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i) acc[i][j][h] = negb ? neg_bits(cc[i * 8]) : cc[i * 8];
+      }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&c_empty);
+    for (int kt = 0; kt < KT; ++kt, ++it) {
+      const int st = it % S;
+      mbar_wait(&full[st], (it / S) & 1u);
+      const double* as = sm + st * Cfg::STAGE;
+      const double* bs = as + Cfg::A_ELEMS;
+#pragma unroll
+      for (int ks = 0; ks < BK; ks += 4) {
+        double af[Cfg::FM], bf[Cfg::FN];
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i) af[i] = as[(ks + lc) * Cfg::LDA_S + wm * Cfg::WTM + i * 8 + lr];
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) {
+          const int n = wn * Cfg::WTN + j * 8 + lr;
+          bf[j] = TB ? bs[(ks + lc) * Cfg::LDB_S + n] : bs[n * Cfg::LDB_S + ks + lc];
+        }
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < Cfg::FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gn = n0 + wn * Cfg::WTN + j * 8 + lc * 2 + h;
+        double* cc = C + (long long)gn * ldc + m0 + wm * Cfg::WTM + lr;
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i)
+          if (gn < N && m0 + wm * Cfg::WTM + i * 8 + lr < M) cc[i * 8] = negb ? neg_bits(acc[i][j][h]) : acc[i][j][h];
+      }
+  }
+}
+
+template <bool TB>
+static int launch_rankk_tilec(cudaStream_t st, const GemmDesc& d, int sms) {
+  constexpr int S = 3;
+  using Cfg = DgemmWsCfg<false, TB, S>;
+  using CC = RankkTileCCfg<TB, S>;
+  CUtensorMap tA, tB, tC;
+  if (make_tmap_2d(&tA, d.A, d.m, d.k, d.lda, Cfg::LDA_S, Cfg::BK)) return -1;
+  if (TB) {
+    if (make_tmap_2d(&tB, d.B, d.n, d.k, d.ldb, Cfg::LDB_S, Cfg::BK)) return -1;
+  } else if (make_tmap_2d(&tB, d.B, d.k, d.n, d.ldb, Cfg::LDB_S, Cfg::BN)) {
+    return -1;
+  }
+  if (make_tmap_2d(&tC, d.C, d.m, d.n, d.ldc, CC::LDC_S, Cfg::BN)) return -1;
+  auto kern = rankk_tilec_kernel<TB, S>;
+  DC_CUDA_TRY((cudaError_t)func_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM_BYTES));
+  const long long ntiles = (long long)((d.m + Cfg::BM - 1) / Cfg::BM) * ((d.n + Cfg::BN - 1) / Cfg::BN);
+  const int grid = (int)std::max(1LL, std::min<long long>(ntiles, sms));
+  kern<<<grid, Cfg::THREADS, CC::SMEM_BYTES, st>>>(d, tA, tB, tC);
+  note_launch();
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
 }
 
 template <bool TB>
@@ -1496,10 +1642,19 @@ static int try_rankk(cudaStream_t st, bool ta, bool tb, const GemmDesc& d) {
     const int r = try_dgemm_ws(st, ta, tb, &b);
     if (r >= 0) return r;
   }
-  // K > 64 (the 128-wide CWY updates of ORMBR / GEQRF / ORGQR): persistent
-  // 128 x 64-tile TMA kernel with folded C (8192^2 K = 128: 24.7 -> 29.0
-  // TFLOP/s, C2 ORMBR 84.6 -> 79.7 ms); at K = 64 it does not beat the
-  // streaming kernel (21.0 vs 21.5), which keeps the GEBRD trailing update.
+  // Every rank-k update with beta = 1, alpha = +-1 (GEBRD A -= P Q^T at K = 64,
+  // the 128-wide CWY updates of ORMBR / GEQRF / ORGQR at K = 128): the
+  // persistent 128 x 64-tile TMA kernel with the C tile staged in shared memory
+  // (8160^2 K = 64: 21.5 -> 29.7 TFLOP/s; 8192^2 K = 128: 24.9 -> 32.9; C2
+  // 639 -> 626 ms; tools/rankk_tile_ab.py).  dcsvd_debug_dgemm_ws(3): the
+  // register-prefetch variant; (0): the cp.async streaming kernel.
+  const bool fold_ok = d.beta == 1.0 && (d.alpha == 1.0 || d.alpha == -1.0);
+  if (g_dgemm_ws && g_dgemm_ws != 3 && fold_ok &&
+      !((reinterpret_cast<uintptr_t>(d.A) & 15) || (reinterpret_cast<uintptr_t>(d.B) & 15) ||
+        (reinterpret_cast<uintptr_t>(d.C) & 15) || (d.lda & 1) || (d.ldb & 1) || (d.ldc & 1))) {
+    const int r = tb ? launch_rankk_tilec<true>(st, d, sms) : launch_rankk_tilec<false>(st, d, sms);
+    if (r >= 0) return r;
+  }
   if (g_dgemm_ws && (d.k > 64 || g_dgemm_ws == 3) && d.beta == 1.0 && (d.alpha == 1.0 || d.alpha == -1.0) &&
       !((reinterpret_cast<uintptr_t>(d.A) & 15) || (reinterpret_cast<uintptr_t>(d.B) & 15) || (d.lda & 1) || (d.ldb & 1))) {
     const int r = tb ? launch_rankk_tile<true>(st, d, sms) : launch_rankk_tile<false>(st, d, sms);

@@ -447,12 +447,12 @@ def test_rank_k_update_kernel(cuda, k, tb, m, ab):
     assert (c - ref).abs().max().item() <= 1e-12 * max(k, 1)
 
 
-@pytest.mark.parametrize("ws", [(1, 1), (0, 1), (0, 0)])
+@pytest.mark.parametrize("ws", [(1, 1), (3, 1), (0, 1), (0, 0)])
 def test_rank_k_kernels_agree_on_pipeline_shapes(cuda, ws):
     """The ORMBR-shaped rank-128 update (8192 x 4096, C -= Y X) through the
-    persistent TMA tile kernel (default), the 3-group TMA kernel
-    (dcsvd_debug_dgemm_ws(0)) and the cp.async streaming kernel (both off),
-    against torch."""
+    persistent TMA tile kernel with C staged in shared memory (default), its
+    register-prefetch variant (3), the 3-group TMA kernel (dgemm_ws 0) and the
+    cp.async streaming kernel (both off), against torch."""
     g = _g()
     lib = _lib_handle()
     torch.manual_seed(5)

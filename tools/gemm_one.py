@@ -7,6 +7,7 @@ lib = _lib.load_library(); h = _lib.handle(); st = _lib.stream_ptr()
 m, n, k, ta, tb = (int(x) for x in sys.argv[1:6])
 reps = int(sys.argv[6]) if len(sys.argv) > 6 else 3
 lib.dcsvd_debug_ws_flags(int(os.environ.get('WS_FLAGS', '0')))
+lib.dcsvd_debug_dgemm_ws(int(os.environ.get('DGEMM_WS', '1')))
 A = torch.randn(m if ta else k, k if ta else m, dtype=torch.float64, device="cuda").t()
 B = torch.randn(k if tb else n, n if tb else k, dtype=torch.float64, device="cuda").t()
 C = torch.randn(n, m, dtype=torch.float64, device="cuda").t()
