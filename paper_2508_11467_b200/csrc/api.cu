@@ -31,6 +31,7 @@ extern int g_gemm_route;
 extern int g_rankk_ws;
 extern int g_dgemm_ws;
 extern int g_cwy_split_mode;
+int g_ts_qr_nb = 0;   // debug: QR panel width of the TS pre-step (0 = options.qr_block)
 int g_ts_literal = 1;  // TS recombination: 1 = ORGQR + GEMM (driver.py:141-142), 0 = fused reflector apply
 int set_ws_flags(int f);
 thread_local dcsvd_ctx* t_cur = nullptr;
@@ -314,7 +315,7 @@ int gesdd_tall(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* 
   double* tau = pool_take<double>(h, 1, n);
   double* R = pool_take<double>(h, 1, (size_t)n * n);
   pt.mark(PH_GEQRF);
-  rc = geqrf_run(h, st, m, n, A, lda, tau, o.qr_block);
+  rc = geqrf_run(h, st, m, n, A, lda, tau, g_ts_qr_nb > 0 ? g_ts_qr_nb : o.qr_block);
   if (rc) return rc;
   triu_copy_kernel<<<std::min<long long>(148 * 8, (n * n + 255) / 256), 256, 0, st>>>((int)n, A, lda, R, n);
   note_launch();
@@ -406,6 +407,10 @@ int dcsvd_debug_gemm_route(int mode) {
   return 0;
 }
 
+int dcsvd_debug_ts_qr_nb(int nb) {
+  dc::g_ts_qr_nb = nb;
+  return 0;
+}
 int dcsvd_debug_ts_literal(int on) {
   dc::g_ts_literal = on;
   return 0;
