@@ -1117,3 +1117,36 @@ def test_bdc_merge_products_tma_vs_cpasync(cuda, n):
         lib.dcsvd_debug_dgemm_ws(1)
     assert torch.equal(r0.dvals, r1.dvals)
     assert torch.equal(r0.w, r1.w) and torch.equal(r0.qfull, r1.qfull)
+
+
+@pytest.mark.parametrize("shape", [(700, 700), (1536, 1024), (4000, 600)])
+def test_gesdd_c_abi_odd_leading_dimensions(cuda, shape):
+    """dcsvd_gesdd through the C ABI with caller buffers whose leading
+    dimensions are odd (ld = rows + 1): the TMA kernels cannot map such
+    operands and must fall back (rank-k updates on U / V^T, TS recombination)
+    with the same accuracy."""
+    import ctypes
+    from paper_2508_11467_b200 import _lib
+    g = _g()
+    m, n = shape
+    k = min(m, n)
+    a = g.generate_matrix(g.MatrixSpec("random", m, n, seed=m + n), device=True)
+    lda, ldu, ldvt = m + 1, m + 1, k + 1
+    A = torch.zeros(n, lda, dtype=torch.float64, device=cuda)
+    A[:, :m] = a.t()
+    U = torch.zeros(k, ldu, dtype=torch.float64, device=cuda)
+    VT = torch.zeros(n, ldvt, dtype=torch.float64, device=cuda)
+    S = torch.zeros(k, dtype=torch.float64, device=cuda)
+    lib = _lib.load_library()
+    h = _lib.handle()
+    rc = lib.dcsvd_gesdd(h, m, n, _lib.ptr(A), lda, _lib.ptr(S), _lib.ptr(U), ldu, _lib.ptr(VT), ldvt, None, None,
+                         _lib.stream_ptr())
+    _lib.check(rc, h)
+    u = U[:, :m].t()
+    vt = VT[:, :k].t()
+    ref = g.gesdd(a)
+    assert (S - ref.sigma).abs().max().item() <= SIG_TOL * max(m, n) * ref.sigma[0].item()
+    eye = torch.eye(k, dtype=torch.float64, device=cuda)
+    assert torch.linalg.matrix_norm(a - (u * S) @ vt).item() / torch.linalg.matrix_norm(a).item() / max(m, n) <= RES_TOL
+    assert torch.linalg.matrix_norm(u.t() @ u - eye).item() / k <= ORTH_TOL
+    assert torch.linalg.matrix_norm(vt @ vt.t() - eye).item() / k <= ORTH_TOL
