@@ -30,6 +30,7 @@ extern bool g_labrd_last_two_phase;
 extern int g_gemm_route;
 extern int g_rankk_ws;
 extern int g_dgemm_ws;
+extern int g_dgemm_ws_min_split_tiles;
 extern int g_cwy_split_mode;
 int g_ts_qr_nb = 0;   // debug: QR panel width of the TS pre-step (0 = options.qr_block)
 int g_ts_literal = 1;  // TS recombination: 1 = ORGQR + GEMM (driver.py:141-142), 0 = fused reflector apply
@@ -432,6 +433,10 @@ int dcsvd_debug_gemm_stack(dcsvd_handle h, const void* descs, int ndesc, int max
 }
 int dcsvd_debug_cwy_split(int mode) {
   dc::g_cwy_split_mode = mode;
+  return 0;
+}
+int dcsvd_debug_dgemm_ws_min(int tiles) {
+  dc::g_dgemm_ws_min_split_tiles = tiles;
   return 0;
 }
 int dcsvd_debug_dgemm_ws(int on) {
