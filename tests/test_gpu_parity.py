@@ -1072,7 +1072,7 @@ def test_secular_vectors_match_oracle(cuda):
 
 @pytest.mark.parametrize("ta", [False, True])
 @pytest.mark.parametrize("tb", [False, True])
-@pytest.mark.parametrize("shape", [(1000, 2000, 300), (1537, 1029, 97), (128, 9000, 4000)])
+@pytest.mark.parametrize("shape", [(1000, 2000, 300), (1537, 1029, 97), (128, 9000, 4000), (8, 9600, 300), (9600, 8, 300), (300, 9600, 3)])
 def test_tma_gemm_matches_torch(cuda, ta, tb, shape):
     """General GEMMs large enough for the warp-specialized TMA kernel
     (dgemm_ws_kernel: >= 148 output tiles, 16-byte-aligned operands), every
