@@ -182,9 +182,24 @@ static int cwy_split(int sms, int w, long long c_other, long long rows_y) {
   return best;
 }
 
+// G = Y^T Y (w x w output, K = the reflector rows) gets its own split: with
+// one or two 128 x 64 tiles it needs ~74 K-slices to fill the GPU on the TMA
+// GEMM (it ran on 64 x 64 cp.async tiles at ~10 % of peak before).
+constexpr int kMaxGSplit = 74;
+int g_cwy_gsplit = 1;  // debug: 0 = G shares the Z split
+static int cwy_gsplit(int sms, int w, long long rows_y, int S) {
+  if (!g_cwy_gsplit) return S;
+  const long long tg = ((w + 127) / 128) * ((w + 63) / 64);
+  long long sg = (sms + tg - 1) / tg;
+  sg = std::min<long long>(sg, kMaxGSplit);
+  sg = std::min<long long>(sg, std::max<long long>(1, rows_y / 64));
+  return (int)std::max<long long>(sg, S > 1 ? 1 : 1);
+}
+
 static size_t cwy_scratch_doubles(int sms, long long rows_y, long long c_other, int w) {
   const int S = cwy_split(sms, w, c_other, rows_y);
-  return (size_t)S * (size_t)w * (size_t)c_other + (size_t)S * w * w + 2 * (size_t)w * w + 64;
+  const int SG = std::max(S, kMaxGSplit);
+  return (size_t)S * (size_t)w * (size_t)c_other + (size_t)SG * w * w + 2 * (size_t)w * w + 64;
 }
 
 __global__ void copy_tinv_kernel(const double* __restrict__ src, long long lds, int w, double* __restrict__ dst,
@@ -206,18 +221,22 @@ static int cwy_apply(dcsvd_ctx* h, cudaStream_t st, char side, bool trans, bool 
   // split-K so that Z's tiles x S fill the GPU
   if (w > kCwyMaxW) return set_error(h, DCSVD_EINVAL, "CWY block width %d exceeds %d", w, kCwyMaxW);
   const int S = cwy_split(h->sms, w, c_other, rows_y);
+  const int SG = utinv ? 1 : cwy_gsplit(h->sms, w, rows_y, S);
   double* Zp = scratch;
   double* Gp = Zp + (size_t)S * w * c_other;
-  double* Top = Gp + (size_t)S * w * w;
+  double* Top = Gp + (size_t)std::max(S, kMaxGSplit) * w * w;
   double* TinvT = Top + (size_t)w * w;
   // slices of a multiple of 16 rows: every slice base keeps the operands' 16-byte alignment
   const long long kchunk = (((rows_y + S - 1) / S) + 15) & ~15LL;
+  const long long gchunk = (((rows_y + SG - 1) / SG) + 15) & ~15LL;
   // one descriptor each, split over K inside the kernel (slice s -> partial s)
   GemmBatch zb, gb;
   zb.count = 1;
   gb.count = 1;
-  zb.ksplit = gb.ksplit = S;
-  zb.kchunk = gb.kchunk = (int)kchunk;
+  zb.ksplit = S;
+  gb.ksplit = SG;
+  zb.kchunk = (int)kchunk;
+  gb.kchunk = (int)gchunk;
   zb.cslice = (long long)w * c_other;
   gb.cslice = (long long)w * w;
   {
@@ -250,7 +269,7 @@ static int cwy_apply(dcsvd_ctx* h, cudaStream_t st, char side, bool trans, bool 
   } else {
     rc = gemm_launch_batch(st, !ytrans, ytrans, gb);
     if (rc) return rc;
-    cwy_tinv_build_kernel<<<(w * w + 255) / 256, 256, 0, st>>>(Gp, S, w, tau, TinvT, h->d_err);
+    cwy_tinv_build_kernel<<<(w * w + 255) / 256, 256, 0, st>>>(Gp, SG, w, tau, TinvT, h->d_err);
   }
   note_launch();
   rc = tinv_solve_launch(st, TinvT, w, trans, Top);
