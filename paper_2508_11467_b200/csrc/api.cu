@@ -31,6 +31,7 @@ extern int g_gemm_route;
 extern int g_rankk_ws;
 extern int g_dgemm_ws;
 extern int g_dgemm_ws_min_split_tiles;
+extern int g_dgemm_ws_min_tiles;
 extern int g_cwy_split_mode;
 extern int g_cwy_gsplit;
 int g_ts_qr_nb = 0;   // debug: QR panel width of the TS pre-step (0 = options.qr_block)
@@ -438,6 +439,10 @@ int dcsvd_debug_cwy_gsplit(int on) {
 }
 int dcsvd_debug_cwy_split(int mode) {
   dc::g_cwy_split_mode = mode;
+  return 0;
+}
+int dcsvd_debug_dgemm_ws_min_nosplit(int tiles) {
+  dc::g_dgemm_ws_min_tiles = tiles;
   return 0;
 }
 int dcsvd_debug_dgemm_ws_min(int tiles) {

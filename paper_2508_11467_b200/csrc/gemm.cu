@@ -1039,6 +1039,7 @@ __global__ void __launch_bounds__(288, 1)
 }
 
 int g_dgemm_ws_min_split_tiles = 148;  // debug knob (dcsvd_debug_dgemm_ws_min)
+int g_dgemm_ws_min_tiles = 148;        // debug knob (dcsvd_debug_dgemm_ws_min_nosplit)
 int g_dgemm_ws = 1;  // debug: 0 = cp.async kernels only, 2 = rank-k (K > 64) on the non-persistent TMA GEMM, 3 = register-C rank-k tile kernel
 
 // Persistent rank-k update on the TMA GEMM tiles (C <- C -+ A op(B), K <= 128,
@@ -1368,7 +1369,7 @@ static int try_dgemm_ws(cudaStream_t st, bool ta, bool tb, const GemmBatch* b) {
   const long long tiles = (long long)((d.m + 127) / 128) * ((d.n + 63) / 64) * ks;
   // too few tiles for one CTA per SM (split-K products with long slices still
   // beat the 64x64 cp.async config from half a wave: g_dgemm_ws_min_tiles)
-  if (tiles < (ks > 1 ? g_dgemm_ws_min_split_tiles : 148)) return -1;
+  if (tiles < (ks > 1 ? g_dgemm_ws_min_split_tiles : g_dgemm_ws_min_tiles)) return -1;
   if (!ta && !tb) return launch_dgemm_ws<false, false>(st, d, ks, b->kchunk, b->cslice);
   if (!ta && tb) return launch_dgemm_ws<false, true>(st, d, ks, b->kchunk, b->cslice);
   if (ta && !tb) return launch_dgemm_ws<true, false>(st, d, ks, b->kchunk, b->cslice);
