@@ -327,7 +327,7 @@ def run_reference(args):
         val, unit, ms, hib = workload_flops(m_s, n_s) / t / 1e9, "GFLOP/s", t * 1e3, True
         metric = "fp64 SVD (U,S,V) GFLOP/s (28/3 n^3 convention)"
         sample = (f"{who}, {cores} BLAS threads, full SVD of MatrixSpec('random',{m_s},{n_s}) per step; "
-                  "C2 itself took 711.5 s on 8 survey-host threads (BASELINE.md)")
+                  "the full C2 took 563.4 s on a B200 box's 16 host cores (profiles/ref_fullsize_r02.md)")
         cfg = {"workload": desc, "m": m, "n": n, "sample_m": m_s, "sample_n": n_s}
     line = {
         "impl": "reference", "metric": metric, "value": val,
