@@ -1150,3 +1150,19 @@ def test_gesdd_c_abi_odd_leading_dimensions(cuda, shape):
     assert torch.linalg.matrix_norm(a - (u * S) @ vt).item() / torch.linalg.matrix_norm(a).item() / max(m, n) <= RES_TOL
     assert torch.linalg.matrix_norm(u.t() @ u - eye).item() / k <= ORTH_TOL
     assert torch.linalg.matrix_norm(vt @ vt.t() - eye).item() / k <= ORTH_TOL
+
+
+@pytest.mark.parametrize("shape", [(300000, 1, 64, False), (256, 1100, 128, True), (262144, 2, 5, False), (1000, 300, 128, True)])
+def test_rank_k_degenerate_shapes(cuda, shape):
+    """Rank-k updates at the edges of the TMA tile kernel's routing (one or two
+    output columns, the minimum 256 rows, K = 5): zero-filled boxes past the
+    tensor, short tiles; against torch fp64."""
+    g = _g()
+    m, n, k, tb = shape
+    torch.manual_seed(m + n + k)
+    a = torch.randn(k, m, dtype=torch.float64, device=cuda).t()
+    b = torch.randn(k, n, dtype=torch.float64, device=cuda).t() if tb else torch.randn(n, k, dtype=torch.float64, device=cuda).t()
+    c = torch.randn(n, m, dtype=torch.float64, device=cuda).t()
+    ref = c - a @ (b.t() if tb else b)
+    g.matmul_accumulate(-1.0, a, False, b, tb, 1.0, c)
+    assert (c - ref).abs().max().item() <= 1e-12 * max(k, 1) * max(1.0, ref.abs().max().item())
