@@ -34,6 +34,7 @@ extern int g_dgemm_ws_min_split_tiles;
 extern int g_dgemm_ws_min_tiles;
 extern int g_cwy_split_mode;
 extern int g_cwy_gsplit;
+extern int g_qr_outer;
 int g_ts_qr_nb = 0;   // debug: QR panel width of the TS pre-step (0 = options.qr_block)
 int g_ts_literal = 1;  // TS recombination: 1 = ORGQR + GEMM (driver.py:141-142), 0 = fused reflector apply
 int set_ws_flags(int f);
@@ -432,6 +433,10 @@ int dcsvd_debug_gemm_stack(dcsvd_handle h, const void* descs, int ndesc, int max
   cudaFree(dd);
   if (rc) return rc;
   return e == cudaSuccess ? 0 : dc_cuda_fail(e, "gemm_stack");
+}
+int dcsvd_debug_qr_outer(int w) {
+  dc::g_qr_outer = w;
+  return 0;
 }
 int dcsvd_debug_cwy_gsplit(int on) {
   dc::g_cwy_gsplit = on;

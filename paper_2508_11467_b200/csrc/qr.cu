@@ -187,6 +187,7 @@ static int cwy_split(int sms, int w, long long c_other, long long rows_y) {
 // GEMM (it ran on 64 x 64 cp.async tiles at ~10 % of peak before).
 constexpr int kMaxGSplit = 74;
 int g_cwy_gsplit = 1;  // debug: 0 = G shares the Z split
+int g_qr_outer = 0;    // debug: outer CWY block width of GEQRF (0 = 128; 64: C3 GEQRF 15.0 -> 16.2 ms, 32: 20.2)
 static int cwy_gsplit(int sms, int w, long long rows_y, int S) {
   if (!g_cwy_gsplit) return S;
   const long long tg = ((w + 127) / 128) * ((w + 63) / 64);
@@ -491,7 +492,8 @@ int geqrf_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A
   // are factored and applied inside an outer block of W = nb*ceil(128/nb)
   // columns; the far trailing matrix then takes one W-wide CWY block (DMMA
   // GEMMs with K = W instead of K = nb).
-  const int W = std::min(kCwyMaxW, nb * std::max(1, kCwyMaxW / nb));
+  const int W = g_qr_outer > 0 ? std::min(kCwyMaxW, std::max(nb, g_qr_outer / nb * nb))
+                               : std::min(kCwyMaxW, nb * std::max(1, kCwyMaxW / nb));
   const size_t need = pool_bytes((size_t)m * W, 8) + pool_bytes((size_t)h->sms * 128 + 128, 8) +
                       pool_bytes(cwy_total_scratch(h->sms, m, n, W), 8);
   int rc = pool_reserve(h, 0, need, st);
