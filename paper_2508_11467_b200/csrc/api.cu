@@ -11,6 +11,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "ctx.cuh"
 #include "gemm.cuh"
 #include "launch.cuh"
@@ -199,17 +201,27 @@ __global__ void triu_copy_kernel(int n, const double* __restrict__ A, long long 
   }
 }
 
+// Per-phase CUDA events (phase_profile) and NVTX ranges named after the
+// reference's PHASE_NAMES (driver.py:31) around each phase's enqueue, so an
+// nsys / ncu --nvtx timeline shows the pipeline stages.
 struct PhaseTimer {
   bool on;
   cudaStream_t st;
   cudaEvent_t ev[16];
   int idx[16];
   int cnt = 0;
+  bool nvtx_open = false;
   PhaseTimer(bool on_, cudaStream_t s) : on(on_), st(s) {}
   ~PhaseTimer() {
+    if (nvtx_open) nvtxRangePop();
     for (int i = 0; i < cnt; ++i) cudaEventDestroy(ev[i]);
   }
   void mark(int phase) {  // phase = index into the profile struct (0..5), -1 = end marker
+    static const char* kNames[6] = {"dcsvd:geqrf", "dcsvd:orgqr", "dcsvd:gebrd", "dcsvd:bdcdc", "dcsvd:ormqr+ormlq",
+                                    "dcsvd:gemm"};
+    if (nvtx_open) nvtxRangePop();
+    nvtx_open = phase >= 0 && phase < 6;
+    if (nvtx_open) nvtxRangePushA(kNames[phase]);
     if (!on || cnt >= 16) return;
     cudaEventCreate(&ev[cnt]);
     cudaEventRecord(ev[cnt], st);

@@ -1109,6 +1109,7 @@ __global__ void __launch_bounds__(kG2cThreads, 1) gebd2_cluster_kernel(Gebd2cArg
       double pi, br;
       larfg_scalars(al, part, pi, br);
       const double dr = al - br;
+      __syncthreads();  // every thread has read alpha before it is overwritten by beta (racecheck WAR)
       if (tid == 0) {
         a.taup[k] = pi;
         a.e[k] = br;

@@ -32,3 +32,20 @@ x = g.generate_matrix(g.MatrixSpec("logrand", 40, 30, 1e6, seed=1))
 rep = g.accuracy(x, g.gesdd(x), reference_sigma=g.prescribed_singular_values("logrand", 30, 1e6, seed=1))
 torch.cuda.synchronize()
 print("sanitize_small round-1 additions ok", rep)
+
+# round-2 additions: the TMA kernels (rank-k tile kernel with smem C, warp-specialized
+# long-K GEMM with split-K, BDC gather4 merge products over the workspace stack)
+t = torch.randn(1024, 1024, dtype=torch.float64, device="cuda").t()            # 1024^2 C
+p_ = torch.randn(64, 1024, dtype=torch.float64, device="cuda").t()
+q_ = torch.randn(64, 1024, dtype=torch.float64, device="cuda").t()
+g.matmul_accumulate(-1.0, p_, False, q_, True, 1.0, t)                           # rankk_tilec_kernel, K = 64
+y_ = torch.randn(128, 1024, dtype=torch.float64, device="cuda").t()
+x_ = torch.randn(1024, 128, dtype=torch.float64, device="cuda").t()
+g.matmul_accumulate(-1.0, y_, False, x_, False, 1.0, t)                          # rankk_tilec_kernel, K = 128
+big = torch.randn(9600, 300, dtype=torch.float64, device="cuda").t()            # 300 x 9600
+ya = torch.randn(128, 300, dtype=torch.float64, device="cuda").t()              # 300 x 128
+w_ = torch.zeros(9600, 128, dtype=torch.float64, device="cuda").t()             # 128 x 9600
+g.matmul_accumulate(1.0, ya, True, big, False, 0.0, w_)                         # dgemm_ws_kernel (TA), 150 tiles
+a = g.generate_matrix(g.MatrixSpec("random", 1500, 1500, seed=5), device=True)
+r = g.gesdd(a)                                    # ORMBR CWY split-K products (dgemm_ws), BDC gather4
+print("round-2 done", float(r.sigma[0]))
