@@ -29,6 +29,8 @@ int set_rankk_chunk(int c);
 int set_rankk_bulk(int on);
 int set_rankk_min(long long mn);
 extern bool g_labrd_last_two_phase;
+extern int g_labrd_halfwidth;
+extern long long g_labrd_halfwidth_max;
 extern int g_gemm_route;
 extern int g_rankk_ws;
 extern int g_dgemm_ws;
@@ -503,6 +505,14 @@ int dcsvd_debug_labrd_l2keep(double bytes) {
 /* smallest panel matrix (bytes) that uses the L2 hints (debug / tuning) */
 int dcsvd_debug_labrd_l2keep_min(double bytes) {
   dc::g_labrd_l2keep_min = bytes;
+  return 0;
+}
+
+/* half-width GEBRD panels where they let the two-phase LABRD kernel run (1, default) or never (0);
+   max_elems bounds the view size (m'*n') that gets them (<= 0: no bound); debug / tuning */
+int dcsvd_debug_labrd_halfwidth(int on, long long max_elems) {
+  dc::g_labrd_halfwidth = on;
+  dc::g_labrd_halfwidth_max = max_elems > 0 ? max_elems : (1LL << 62);
   return 0;
 }
 

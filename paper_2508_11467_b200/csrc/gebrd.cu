@@ -1281,6 +1281,33 @@ static LabrdWork labrd_work_take(dcsvd_ctx* h, int pool, long long mp, long long
   return w;
 }
 
+// Does the two-phase kernel's P/Q block cache fit for an mv x nv view with panel width nb?
+static bool labrd2_fits(int mv, int nv, int nb, int G) {
+  for (int cand : {2, 4, 8, 16}) {
+    const int RB = 32 * cand;
+    const int Gr = (mv + RB - 1) / RB;
+    int Gc = std::max(1, G / std::max(Gr, 1));
+    const int CB = (nv + Gc - 1) / Gc;
+    if (Gr > G || CB > 4 * kLabrdThreads) continue;
+    const size_t CBp = (CB + 1) & ~1, NC = (2 * nb + 3) & ~3;
+    const size_t bytes = sizeof(double) * (3 * RB + 3 * CBp + (size_t)kLabrdWarps * RB + (RB + CBp + 2) * NC);
+    if (bytes <= (size_t)kLabrdSmemMax) return true;
+  }
+  return false;
+}
+
+// Panel width for the view: half-width panels where that lets the two-phase
+// kernel (2 grid barriers per column) replace the four-phase one (4 barriers).
+int g_labrd_halfwidth = 1;  // debug: 0 = always the requested width
+long long g_labrd_halfwidth_max = 1LL << 62;  // debug: largest view (elements) given half-width panels
+static int labrd_panel_width(int mv, int nv, int nb, int G) {
+  if (!g_labrd_halfwidth || nb < 32 || labrd2_fits(mv, nv, nb, G)) return nb;
+  if ((long long)mv * nv > g_labrd_halfwidth_max) return nb;
+  if (labrd2_fits(mv, nv, nb / 2, G)) return nb / 2;
+  if (g_labrd_halfwidth >= 2 && labrd2_fits(mv, nv, nb / 4, G)) return nb / 4;  // debug: quarter width
+  return nb;
+}
+
 // One LABRD panel on the mv x nv view Av (bidiag.py:113-165): P (mv x 2nb,
 // ldp) and Q (nv x 2nb, ldq) are zeroed here and filled; only the panel
 // rows/columns of Av change.
@@ -1409,18 +1436,19 @@ int gebrd_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A
   while (n - off > nb && !unblocked && !gebd2c_fits((int)(m - off), (int)(n - off))) {
     const int mv = (int)(m - off), nv = (int)(n - off);
     double* Av = A + off + off * lda;
-    rc = labrd_launch(h, st, mv, nv, Av, lda, nb, d + off, e + off, tauq + off, taup + off, P, mp, Q, np, w);
+    const int nbp = labrd_panel_width(mv, nv, nb, G);  // same reflectors for any width
+    rc = labrd_launch(h, st, mv, nv, Av, lda, nbp, d + off, e + off, tauq + off, taup + off, P, mp, Q, np, w);
     if (rc) return rc;
     // trailing update A[nb:, nb:] -= P[nb:, :] Q[nb:, :]^T  (bidiag.py:195-197)
     GemmDesc gd;
-    gd.m = mv - nb; gd.n = nv - nb; gd.k = 2 * nb;
-    gd.A = P + nb; gd.lda = mp; gd.acol = nullptr;
-    gd.B = Q + nb; gd.ldb = np;
-    gd.C = Av + nb + (long long)nb * lda; gd.ldc = lda; gd.ccol = nullptr;
+    gd.m = mv - nbp; gd.n = nv - nbp; gd.k = 2 * nbp;
+    gd.A = P + nbp; gd.lda = mp; gd.acol = nullptr;
+    gd.B = Q + nbp; gd.ldb = np;
+    gd.C = Av + nbp + (long long)nbp * lda; gd.ldc = lda; gd.ccol = nullptr;
     gd.alpha = -1.0; gd.beta = 1.0;
     rc = gemm_launch(st, false, true, gd);
     if (rc) return rc;
-    off += nb;
+    off += nbp;
   }
   if (gebd2c_fits((int)(m - off), (int)(n - off))) {
     rc = gebd2c_launch(st, A + off + off * lda, lda, (int)(m - off), (int)(n - off), d + off, e + off, tauq + off,

@@ -191,6 +191,30 @@ def test_gebrd_cluster_tail_modes(cuda, golden, mode):
         lib.dcsvd_debug_gebd2_cluster(1)
 
 
+def test_gebrd_halfwidth_panels(cuda):
+    """Mid-size views take 16-wide panels so the two-phase LABRD kernel runs
+    (gebrd.cu labrd_panel_width): same factorization as 32-wide panels up to
+    rounding (the panel width only regroups the trailing updates), and the
+    same singular values through gesdd."""
+    g = _g()
+    lib = _lib_handle()
+    a = g.generate_matrix(g.MatrixSpec("random", 3072, 3000, seed=5), device=True)
+    out = {}
+    try:
+        for mode in (0, 1):
+            lib.dcsvd_debug_labrd_halfwidth(mode, 0)
+            f = g.gebrd_blocked(a.clone())
+            s = g.gesdd(a, g.SVDOptions(want_vectors=False)).sigma
+            s = s.cpu().numpy() if isinstance(s, torch.Tensor) else np.asarray(s)
+            out[mode] = (f.d.abs().cpu().numpy(), f.e.abs().cpu().numpy(), s)
+    finally:
+        lib.dcsvd_debug_labrd_halfwidth(1, 0)
+    sc = float(torch.linalg.norm(a))
+    for i in range(2):
+        assert np.max(np.abs(out[1][i] - out[0][i])) <= 1e-12 * sc
+    assert np.max(np.abs(out[1][2] - out[0][2])) <= SIG_TOL * 3072 * out[0][2][0]
+
+
 def test_gebrd_unblocked_and_panel(cuda):
     g = _g()
     rng = np.random.default_rng(6)
