@@ -30,6 +30,7 @@ int set_rankk_bulk(int on);
 int set_rankk_min(long long mn);
 extern bool g_labrd_last_two_phase;
 extern int g_labrd_halfwidth;
+extern int g_ormbr_pre;
 extern long long g_labrd_halfwidth_max;
 extern int g_gemm_route;
 extern int g_rankk_ws;
@@ -513,6 +514,12 @@ int dcsvd_debug_labrd_l2keep_min(double bytes) {
 int dcsvd_debug_labrd_halfwidth(int on, long long max_elems) {
   dc::g_labrd_halfwidth = on;
   dc::g_labrd_halfwidth_max = max_elems > 0 ? max_elems : (1LL << 62);
+  return 0;
+}
+
+/* ORMBR: op(T) of all full CWY blocks precomputed in batched launches (1, default) or per block (0); debug */
+int dcsvd_debug_ormbr_pre(int on) {
+  dc::g_ormbr_pre = on;
   return 0;
 }
 

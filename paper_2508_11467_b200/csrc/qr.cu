@@ -12,6 +12,8 @@
 // inverts it (so the reference's TRSM becomes one small GEMM X = T Z), then
 // C -= Y X.  The unblocked QR panel is a cooperative kernel that keeps each
 // CTA's row slab of the panel in shared memory for all its columns.
+#include <vector>
+
 #include "ctx.cuh"
 #include "gemm.cuh"
 #include "launch.cuh"
@@ -45,8 +47,12 @@ __global__ void build_y_kernel(int ymode, const double* __restrict__ src, long l
 // (qrblock.py:90-100), column-major into global scratch.
 constexpr int kCwyMaxW = 128;
 
+// (batched over blockIdx.y: block b reads Gp + b gstride, tau + b taustride, writes Tinv + b w^2)
 __global__ void cwy_tinv_build_kernel(const double* __restrict__ Gp, int S, int w, const double* __restrict__ tau,
-                                      double* __restrict__ Tinv, int* err) {
+                                      double* __restrict__ Tinv, int* err, long long gstride = 0, int taustride = 0) {
+  Gp += blockIdx.y * gstride;
+  tau += blockIdx.y * taustride;
+  Tinv += (long long)blockIdx.y * w * w;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= w * w) return;
   const int i = idx % w, l = idx / w;
@@ -68,6 +74,8 @@ constexpr int kTinvSolveWarps = 16;
 __global__ void __launch_bounds__(32 * kTinvSolveWarps) cwy_tinv_solve_kernel(const double* __restrict__ Tinv, int w,
                                                                               int trans, double* __restrict__ Top) {
   extern __shared__ double ts[];  // w x w (ld w); diagonal replaced by its reciprocal
+  Tinv += (long long)blockIdx.y * w * w;  // batched over blockIdx.y (one w x w block each)
+  Top += (long long)blockIdx.y * w * w;
   {
     const int tot = w * w;
     if ((reinterpret_cast<uintptr_t>(Tinv) & 15) == 0) {  // 16-byte staging, 4 loads in flight
@@ -117,11 +125,11 @@ __global__ void __launch_bounds__(32 * kTinvSolveWarps) cwy_tinv_solve_kernel(co
   }
 }
 
-static int tinv_solve_launch(cudaStream_t st, const double* Tinv, int w, bool trans, double* Top) {
+static int tinv_solve_launch(cudaStream_t st, const double* Tinv, int w, bool trans, double* Top, int nbatch = 1) {
   DC_CUDA_TRY((cudaError_t)func_attr(cwy_tinv_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kCwyMaxW * kCwyMaxW * 8));
-  cwy_tinv_solve_kernel<<<(w + kTinvSolveWarps - 1) / kTinvSolveWarps, 32 * kTinvSolveWarps, (size_t)w * w * 8, st>>>(
-      Tinv, w, trans ? 1 : 0, Top);
+  cwy_tinv_solve_kernel<<<dim3((w + kTinvSolveWarps - 1) / kTinvSolveWarps, nbatch), 32 * kTinvSolveWarps,
+                          (size_t)w * w * 8, st>>>(Tinv, w, trans ? 1 : 0, Top);
   note_launch();
   DC_CUDA_TRY(cudaGetLastError());
   return 0;
@@ -217,7 +225,8 @@ __global__ void copy_tinv_kernel(const double* __restrict__ src, long long lds, 
 // built from Y and tau (apply_block_reflector_*, qrblock.py:103-119).
 static int cwy_apply(dcsvd_ctx* h, cudaStream_t st, char side, bool trans, bool ytrans, const double* Y,
                      long long ldy, const double* tau, int w, long long rows_y, double* C, long long ldc,
-                     long long c_other, double* scratch, const double* utinv = nullptr, long long ldt = 0) {
+                     long long c_other, double* scratch, const double* utinv = nullptr, long long ldt = 0,
+                     const double* utop = nullptr) {
   if (rows_y <= 0 || c_other <= 0 || w <= 0) return 0;
   // split-K so that Z's tiles x S fill the GPU
   if (w > kCwyMaxW) return set_error(h, DCSVD_EINVAL, "CWY block width %d exceeds %d", w, kCwyMaxW);
@@ -265,16 +274,20 @@ static int cwy_apply(dcsvd_ctx* h, cudaStream_t st, char side, bool trans, bool 
   if (side == 'L') rc = gemm_launch_batch(st, /*ta=*/!ytrans, /*tb=*/false, zb);
   else rc = gemm_launch_batch(st, false, /*tb=*/ytrans, zb);
   if (rc) return rc;
-  if (utinv) {
+  if (utop) {
+    Top = const_cast<double*>(utop);  // op(T) precomputed by the caller (ormbr_run)
+  } else if (utinv) {
     copy_tinv_kernel<<<(w * w + 255) / 256, 256, 0, st>>>(utinv, ldt, w, TinvT, h->d_err);
   } else {
     rc = gemm_launch_batch(st, !ytrans, ytrans, gb);
     if (rc) return rc;
     cwy_tinv_build_kernel<<<(w * w + 255) / 256, 256, 0, st>>>(Gp, SG, w, tau, TinvT, h->d_err);
   }
-  note_launch();
-  rc = tinv_solve_launch(st, TinvT, w, trans, Top);
-  if (rc) return rc;
+  if (!utop) {
+    note_launch();
+    rc = tinv_solve_launch(st, TinvT, w, trans, Top);
+    if (rc) return rc;
+  }
   const long long zc = (long long)w * c_other;
   if (S > 1) {
     splitk_reduce_kernel<<<grid_for(zc), 256, 0, st>>>(Zp, zc, S);
@@ -566,51 +579,90 @@ int orgqr_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long nrefl, long 
   return 0;
 }
 
+// op(T) of every full-width block depends only on the packed reflectors, so
+// ormbr builds all blocks' Y once and computes G_b = Y_b^T Y_b (batched DMMA
+// GEMM, kPreGSplit K-slices), Tinv_b and op(T_b) in one launch each before the
+// apply loop, instead of three launches per block on the loop's critical path.
+constexpr int kPreGSplit = 4;
+int g_ormbr_pre = 1;  // debug: 0 = per-block T inside the apply loop
+
 int ormbr_run(dcsvd_ctx* h, cudaStream_t st, char vect, bool trans, long long m, long long n, const double* A,
               long long lda, const double* tau, double* C, long long c_rows, long long c_cols, long long ldc,
               int nb) {
   if (nb < 1) return set_error(h, DCSVD_EINVAL, "block width must be >= 1, got %d", nb);
   if (nb > kCwyMaxW) nb = kCwyMaxW;  // same product, grouped in 128-wide compact-WY blocks
-  if (vect == 'Q') {
-    if (c_rows != m) return set_error(h, DCSVD_EINVAL, "C has %lld rows, sequence acts on %lld", c_rows, m);
-    const long long count = n;
-    const size_t need = pool_bytes((size_t)m * nb, 8) + pool_bytes(cwy_total_scratch(h->sms, m, c_cols, nb), 8);
-    int rc = pool_reserve(h, 0, need, st);
-    if (rc) return rc;
-    double* Y = pool_take<double>(h, 0, (size_t)m * nb);
-    double* scr = pool_take<double>(h, 0, cwy_total_scratch(h->sms, m, c_cols, nb));
-    const long long nblk = (count + nb - 1) / nb;
-    for (long long b = 0; b < nblk; ++b) {
-      const long long bi = trans ? b : nblk - 1 - b;  // U1^T front-to-back, U1 back-to-front
-      const long long off = bi * nb;
-      const int w = (int)std::min<long long>(nb, count - off);
-      const long long rows = m - off;
-      build_y_kernel<<<grid_for(rows * w), 256, 0, st>>>(0, A + off + off * lda, lda, tau + off, (int)rows, w, Y);
-      note_launch();
-      rc = cwy_apply(h, st, 'L', trans, false, Y, rows, tau + off, w, rows, C + off, ldc, c_cols, scr);
+  if (vect != 'Q' && vect != 'P') return set_error(h, DCSVD_EINVAL, "vect must be 'Q' or 'P'");
+  const bool isq = vect == 'Q';
+  if (isq && c_rows != m) return set_error(h, DCSVD_EINVAL, "C has %lld rows, sequence acts on %lld", c_rows, m);
+  if (!isq && c_cols != n) return set_error(h, DCSVD_EINVAL, "C has %lld columns, sequence acts on %lld", c_cols, n);
+  const long long count = isq ? n : (n > 0 ? n - 1 : 0);  // reflectors
+  const long long rows0 = isq ? m : n - 1;                 // rows of block 0's reflectors
+  const long long c_other = isq ? c_cols : c_rows;
+  const long long nblk = (count + nb - 1) / nb;
+  if (nblk == 0) return 0;
+  const long long nfull = g_ormbr_pre ? count / nb : 0;     // blocks with precomputed op(T)
+  std::vector<long long> yoff(nblk + 1, 0);
+  for (long long b = 0; b < nblk; ++b) yoff[b + 1] = yoff[b] + (rows0 - b * nb) * nb;
+  const size_t ww = (size_t)nb * nb;
+  const size_t need = pool_bytes((size_t)yoff[nblk], 8) + pool_bytes(cwy_total_scratch(h->sms, rows0, c_other, nb), 8) +
+                      (nfull ? pool_bytes((size_t)nfull * kPreGSplit * ww, 8) + 2 * pool_bytes((size_t)nfull * ww, 8)
+                             : 0);
+  int rc = pool_reserve(h, 0, need, st);
+  if (rc) return rc;
+  double* Yall = pool_take<double>(h, 0, (size_t)yoff[nblk]);
+  double* scr = pool_take<double>(h, 0, cwy_total_scratch(h->sms, rows0, c_other, nb));
+  double* Gall = nfull ? pool_take<double>(h, 0, (size_t)nfull * kPreGSplit * ww) : nullptr;
+  double* Tinv = nfull ? pool_take<double>(h, 0, (size_t)nfull * ww) : nullptr;
+  double* Top = nfull ? pool_take<double>(h, 0, (size_t)nfull * ww) : nullptr;
+  // Y ('Q': rows x w, ld rows) / Y^T ('P': w x rows, ld w) of every block
+  auto block_rows = [&](long long bi) { return rows0 - bi * nb; };
+  auto block_w = [&](long long bi) { return (int)std::min<long long>(nb, count - bi * nb); };
+  for (long long bi = 0; bi < nblk; ++bi) {
+    const long long off = bi * nb, rows = block_rows(bi);
+    const int w = block_w(bi);
+    const double* src = isq ? A + off + off * lda : A + off + (off + 1) * lda;
+    build_y_kernel<<<grid_for(rows * w), 256, 0, st>>>(isq ? 0 : 1, src, lda, tau + off, (int)rows, w, Yall + yoff[bi]);
+    note_launch();
+  }
+  if (nfull) {
+    for (long long b0 = 0; b0 < nfull; b0 += kMaxBatchDesc) {
+      GemmBatch gb;
+      gb.count = (int)std::min<long long>(kMaxBatchDesc, nfull - b0);
+      gb.ksplit = kPreGSplit;
+      gb.kchunk = (int)((((block_rows(b0) + kPreGSplit - 1) / kPreGSplit) + 15) & ~15LL);
+      gb.cslice = (long long)ww;
+      for (int i = 0; i < gb.count; ++i) {
+        const long long bi = b0 + i;
+        GemmDesc g;
+        g.acol = nullptr; g.ccol = nullptr; g.alpha = 1.0; g.beta = 0.0;
+        g.m = nb; g.n = nb; g.k = (int)block_rows(bi);
+        g.A = Yall + yoff[bi]; g.B = Yall + yoff[bi];
+        g.lda = g.ldb = isq ? block_rows(bi) : nb;
+        g.C = Gall + (size_t)bi * kPreGSplit * ww; g.ldc = nb;
+        gb.d[i] = g;
+      }
+      rc = isq ? gemm_launch_batch(st, true, false, gb) : gemm_launch_batch(st, false, true, gb);
       if (rc) return rc;
     }
-  } else if (vect == 'P') {
-    if (c_cols != n) return set_error(h, DCSVD_EINVAL, "C has %lld columns, sequence acts on %lld", c_cols, n);
-    const long long count = n > 0 ? n - 1 : 0;
-    const size_t need = pool_bytes((size_t)n * nb, 8) + pool_bytes(cwy_total_scratch(h->sms, n, c_rows, nb), 8);
-    int rc = pool_reserve(h, 0, need, st);
+    cwy_tinv_build_kernel<<<dim3((unsigned)((ww + 255) / 256), (unsigned)nfull), 256, 0, st>>>(
+        Gall, kPreGSplit, nb, tau, Tinv, h->d_err, (long long)kPreGSplit * ww, nb);
+    note_launch();
+    rc = tinv_solve_launch(st, Tinv, nb, trans, Top, (int)nfull);
     if (rc) return rc;
-    double* Yt = pool_take<double>(h, 0, (size_t)n * nb);
-    double* scr = pool_take<double>(h, 0, cwy_total_scratch(h->sms, n, c_rows, nb));
-    const long long nblk = (count + nb - 1) / nb;
-    for (long long b = 0; b < nblk; ++b) {
-      const long long bi = trans ? nblk - 1 - b : b;  // V1^T back-to-front, V1 front-to-back
-      const long long off = bi * nb;
-      const int w = (int)std::min<long long>(nb, count - off);
-      const long long rows = n - off - 1;
-      build_y_kernel<<<grid_for(rows * w), 256, 0, st>>>(1, A + off + (off + 1) * lda, lda, tau + off, (int)rows, w, Yt);
-      note_launch();
-      rc = cwy_apply(h, st, 'R', trans, true, Yt, w, tau + off, w, rows, C + (off + 1) * ldc, ldc, c_rows, scr);
-      if (rc) return rc;
-    }
-  } else {
-    return set_error(h, DCSVD_EINVAL, "vect must be 'Q' or 'P'");
+  }
+  for (long long b = 0; b < nblk; ++b) {
+    // 'Q': U1^T front-to-back, U1 back-to-front; 'P': V1^T back-to-front, V1 front-to-back
+    const long long bi = (isq == trans) ? b : nblk - 1 - b;
+    const long long off = bi * nb, rows = block_rows(bi);
+    const int w = block_w(bi);
+    const double* utop = bi < nfull ? Top + (size_t)bi * ww : nullptr;
+    if (isq)
+      rc = cwy_apply(h, st, 'L', trans, false, Yall + yoff[bi], rows, tau + off, w, rows, C + off, ldc, c_cols, scr,
+                     nullptr, 0, utop);
+    else
+      rc = cwy_apply(h, st, 'R', trans, true, Yall + yoff[bi], w, tau + off, w, rows, C + (off + 1) * ldc, ldc, c_rows,
+                     scr, nullptr, 0, utop);
+    if (rc) return rc;
   }
   DC_CUDA_TRY(cudaGetLastError());
   return 0;
