@@ -693,36 +693,50 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd2_kernel(LabrdArgs a) {
       double w[RPL];
 #pragma unroll
       for (int i = 0; i < RPL; ++i) w[i] = sh_c[lane + 32 * i];
-      // A^T c over the block (rows > k, columns > k), two columns per warp step
+      // A^T c over the block (rows > k, columns > k): NC columns per warp step
+      // (loads of all NC columns in flight), the NC lane partials reduced by a
+      // butterfly reduce-scatter (NC - 1 + 5 - log2 NC shuffles instead of 5 NC)
+      constexpr int NC = RPL >= 16 ? 2 : (RPL >= 8 ? 4 : 8);
       const int jstart = max(bc0, k + 1);
-      for (int j = jstart + warp; j < bc1; j += 2 * kLabrdWarps) {
-        const int j2 = j + kLabrdWarps;
-        const bool has2 = j2 < bc1;
-        const double* col0 = A + (long long)j * lda;
-        const double* col1 = A + (long long)(has2 ? j2 : j) * lda;
-        double x0[RPL], x1[RPL];
+      for (int jb = jstart + warp; jb < bc1; jb += NC * kLabrdWarps) {
+        double v[NC];
 #pragma unroll
-        for (int i = 0; i < RPL; ++i) {
-          const int rw = br0 + lane + 32 * i;
-          const bool ok = rw < br1;
-          x0[i] = ok ? col0[rw] : 0.0;
-          x1[i] = ok ? col1[rw] : 0.0;
-        }
-        double s0 = 0.0, s1 = 0.0;
+        for (int c = 0; c < NC; ++c) {
+          const int j = jb + c * kLabrdWarps;
+          const double* col = A + (long long)(j < bc1 ? j : jb) * lda;
+          double x[RPL];
 #pragma unroll
-        for (int i = 0; i < RPL; ++i) {
-          s0 += x0[i] * w[i];
-          s1 += x1[i] * w[i];
-        }
+          for (int i = 0; i < RPL; ++i) {
+            const int rw = br0 + lane + 32 * i;
+            x[i] = (rw < br1 && j < bc1) ? col[rw] : 0.0;
+          }
+          double sc = 0.0;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-          s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+          for (int i = 0; i < RPL; ++i) sc += x[i] * w[i];
+          v[c] = sc;
         }
-        if (lane == 0) {
-          a.py[(long long)gr * a.ldpy + j] = s0 - sh_cq[j - bc0];
-          if (has2) a.py[(long long)gr * a.ldpy + j2] = s1 - sh_cq[j2 - bc0];
+        // reduce-scatter: after the halving steps lane l holds column
+        // cl = bits (l>>4, l>>3, l>>2) (top log2 NC of them) summed over the
+        // lanes that share those bits; then full xor reductions
+#pragma unroll
+        for (int h = NC / 2, off = 16; h >= 1; h >>= 1, off >>= 1) {
+          const bool up = (lane & off) != 0;
+#pragma unroll
+          for (int c = 0; c < h; ++c) {
+            const double send = up ? v[c] : v[c + h];
+            const double keep = up ? v[c + h] : v[c];
+            v[c] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+          }
         }
+        constexpr int LOGNC = NC == 2 ? 1 : (NC == 4 ? 2 : 3);
+#pragma unroll
+        for (int off = 16 >> LOGNC; off > 0; off >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
+        int cl = 0;
+#pragma unroll
+        for (int b = 0; b < LOGNC; ++b) cl |= ((lane >> (4 - b)) & 1) << (LOGNC - 1 - b);
+        const int j = jb + cl * kLabrdWarps;
+        if ((lane & ((16 >> LOGNC) * 2 - 1)) == 0 && j < bc1)
+          a.py[(long long)gr * a.ldpy + j] = v[0] - sh_cq[j - bc0];
       }
     }
     tmark(a, tb + 3);
