@@ -551,6 +551,26 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd4_kernel(LabrdArgs a) {
 // columns in shared memory; owners (gc == 0 for rows, gr == 0 for columns)
 // write them back.  Values produced in a phase are read by other CTAs only
 // after the next barrier.  Used when the P/Q block caches fit (small panels).
+// Butterfly reduce-scatter of four per-lane partials v[q] (q = 0..3): returns
+// in every lane the warp total of v[q] for q = 2 ((lane >> 4) & 1) + ((lane >> 3) & 1)
+// (valid in all lanes; lanes with (lane & 7) == 0 are the natural writers).
+// 3 + 3 shuffles instead of 4 x 5; fixed order, deterministic.
+__device__ __forceinline__ double warp_reduce4_scatter(double (&v)[4], int lane) {
+#pragma unroll
+  for (int h = 2, off = 16; h >= 1; h >>= 1, off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int c = 0; c < h; ++c) {
+      const double send = up ? v[c] : v[c + h];
+      const double keep = up ? v[c + h] : v[c];
+      v[c] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+#pragma unroll
+  for (int off = 4; off > 0; off >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
+  return v[0];
+}
+
 template <int RPL>
 __global__ void __launch_bounds__(kLabrdThreads, 1) labrd2_kernel(LabrdArgs a) {
   extern __shared__ double dsm[];
@@ -657,13 +677,23 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd2_kernel(LabrdArgs a) {
     part = block_sum(part, sh_red);  // also publishes sh_c / Pc / Qc / sh_row
     if (rowowner && tid == 0) a.normc[gr] = part;
     tmark(a, tb + 1);
-    // local P^T c over the block rows, t < 2k (warp per t)
-    for (int t = warp; t < 2 * k; t += kLabrdWarps) {
-      double s = 0.0;
+    // local P^T c over the block rows, t < 2k: warp w handles t = w + 16 q
+    // (q < 4, 2k <= 62) together, one reduce-scatter for the four sums
+    {
+      double v[4];
 #pragma unroll
-      for (int i = 0; i < RPL; ++i) s += Pc[lane + 32 * i + t * LP] * sh_c[lane + 32 * i];
-      s = warp_sum(s);
-      if (lane == 0) sh_pl[t] = s;
+      for (int q = 0; q < 4; ++q) {
+        const int t = warp + kLabrdWarps * q;
+        double s = 0.0;
+        if (t < 2 * k) {
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) s += Pc[lane + 32 * i + t * LP] * sh_c[lane + 32 * i];
+        }
+        v[q] = s;
+      }
+      const double tot = warp_reduce4_scatter(v, lane);
+      const int t = warp + kLabrdWarps * (2 * ((lane >> 4) & 1) + ((lane >> 3) & 1));
+      if ((lane & 7) == 0 && t < 2 * k) sh_pl[t] = tot;
     }
     __syncthreads();
     // Q-correction of the partial A^T c and E = Q[:, :2k-1] P[k, :2k-1]^T for
@@ -811,13 +841,21 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd2_kernel(LabrdArgs a) {
     if (colowner && tid == 0) a.normr[gc] = part;
     tmark(a, tb + 5);
     const int jlo = max(bc0, k + 2);
-    // local Q^T r over the block columns (> k+1), t < 2k+1 (warp per t)
-    for (int t = warp; t < ty + 1; t += kLabrdWarps) {
-      double s = 0.0;
-#pragma unroll 4
-      for (int jj = jlo - bc0 + lane; jj < ncb; jj += 32) s += Qc[jj + t * LQ] * sh_r[jj];
-      s = warp_sum(s);
-      if (lane == 0) sh_pl[t] = s;
+    // local Q^T r over the block columns (> k+1), t < 2k+1 (<= 63): warp w
+    // handles t = w + 16 q (q < 4) in one pass over the columns
+    {
+      double v[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int jj = jlo - bc0 + lane; jj < ncb; jj += 32) {
+        const double rj = sh_r[jj];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int t = warp + kLabrdWarps * q;
+          if (t < ty + 1) v[q] += Qc[jj + t * LQ] * rj;
+        }
+      }
+      const double tot = warp_reduce4_scatter(v, lane);
+      const int t = warp + kLabrdWarps * (2 * ((lane >> 4) & 1) + ((lane >> 3) & 1));
+      if ((lane & 7) == 0 && t < ty + 1) sh_pl[t] = tot;
     }
     __syncthreads();
     // P-correction of the partial A r and D = P[:, :2k] Q[k+1, :2k]^T for the
@@ -844,30 +882,30 @@ __global__ void __launch_bounds__(kLabrdThreads, 1) labrd2_kernel(LabrdArgs a) {
     tmark(a, tb + 6);
     {
       // A r over the block (rows > k, columns > k+1), descending column order
-      // (snake against the A^T c pass), two columns per warp step
+      // (snake against the A^T c pass), NCB columns per warp step
+      constexpr int NCB = RPL >= 8 ? 2 : (RPL >= 4 ? 4 : 8);
       double acc[RPL];
 #pragma unroll
       for (int i = 0; i < RPL; ++i) acc[i] = 0.0;
       const int nj = bc1 - jlo;
-      for (int jj = nj - 1 - warp; jj >= 0; jj -= 2 * kLabrdWarps) {
-        const int j = jlo + jj;
-        const int jj2 = jj - kLabrdWarps;
-        const bool has2 = jj2 >= 0;
-        const int j2 = has2 ? jlo + jj2 : j;
-        const double u0 = sh_r[j - bc0];
-        const double u1 = has2 ? sh_r[j2 - bc0] : 0.0;
-        const double* col0 = A + (long long)j * lda;
-        const double* col1 = A + (long long)j2 * lda;
-        double x0[RPL], x1[RPL];
+      for (int jj = nj - 1 - warp; jj >= 0; jj -= NCB * kLabrdWarps) {
+        double x[NCB][RPL], u[NCB];
 #pragma unroll
-        for (int i = 0; i < RPL; ++i) {
-          const int rw = br0 + lane + 32 * i;
-          const bool ok = rw < br1;
-          x0[i] = ok ? col0[rw] : 0.0;
-          x1[i] = ok ? col1[rw] : 0.0;
+        for (int c = 0; c < NCB; ++c) {
+          const int jc = jj - c * kLabrdWarps;
+          const int j = jlo + (jc >= 0 ? jc : jj);
+          u[c] = jc >= 0 ? sh_r[j - bc0] : 0.0;
+          const double* col = A + (long long)j * lda;
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) {
+            const int rw = br0 + lane + 32 * i;
+            x[c][i] = (rw < br1 && jc >= 0) ? col[rw] : 0.0;
+          }
         }
 #pragma unroll
-        for (int i = 0; i < RPL; ++i) acc[i] += x0[i] * u0 + x1[i] * u1;
+        for (int c = 0; c < NCB; ++c)
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) acc[i] += x[c][i] * u[c];
       }
 #pragma unroll
       for (int i = 0; i < RPL; ++i) sh_acc[warp * RB + lane + 32 * i] = acc[i];
