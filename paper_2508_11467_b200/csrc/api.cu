@@ -21,6 +21,7 @@ namespace dc {
 std::atomic<long long> g_launch_count{0};
 extern unsigned long long* g_labrd_tlog;
 extern int g_labrd_gmax;
+extern int g_labrd2_rpl;
 extern double g_labrd_l2keep;
 extern double g_labrd_l2keep_min;
 extern int g_gebd2_cluster;
@@ -520,6 +521,12 @@ int dcsvd_debug_labrd_halfwidth(int on, long long max_elems) {
 /* ORMBR: op(T) of all full CWY blocks precomputed in batched launches (1, default) or per block (0); debug */
 int dcsvd_debug_ormbr_pre(int on) {
   dc::g_ormbr_pre = on;
+  return 0;
+}
+
+/* force the two-phase LABRD geometry (rows per lane 2/4/8/16; 0 = automatic; debug / tuning) */
+int dcsvd_debug_labrd2_rpl(int rpl) {
+  dc::g_labrd2_rpl = rpl;
   return 0;
 }
 

@@ -1364,6 +1364,7 @@ static int labrd_panel_width(int mv, int nv, int nb, int G) {
 // ldp) and Q (nv x 2nb, ldq) are zeroed here and filled; only the panel
 // rows/columns of Av change.
 int g_labrd_gmax = 0;  // debug: cap on the LABRD grid (0 = all SMs)
+int g_labrd2_rpl = 0;  // debug: rows per lane of the two-phase kernel (0 = the fitting one with most CTAs)
 // bytes of each large-panel GEMV pass kept in L2 with evict_last, the rest evict_first
 // (tools/labrd_l2keep_ab.py at 8192^2: GEBRD 539 -> 532 ms for 16-24 MB; 64+ MB is slower)
 double g_labrd_l2keep = 20.0 * (1 << 20);
@@ -1403,12 +1404,16 @@ static int labrd_launch(dcsvd_ctx* h, cudaStream_t st, int mv, int nv, double* A
   int rpl = 16;
   size_t smem = 0;
   for (int cand : {2, 4, 8, 16}) {
+    if (g_labrd2_rpl && cand != g_labrd2_rpl) continue;  // debug: force one geometry
     int Gr, Gc, CB;
     geom(cand, Gr, Gc, CB);
     if (Gr > G || CB > 4 * kLabrdThreads) continue;
     const size_t RB = 32 * cand, CBp = (CB + 1) & ~1, NC = (2 * nb + 3) & ~3;
     const size_t bytes = sizeof(double) * (3 * RB + 3 * CBp + (size_t)kLabrdWarps * RB + (RB + CBp + 2) * NC);
-    if (bytes <= (size_t)kLabrdSmemMax && (!two_phase || Gr * Gc > la.Gr * la.Gc)) {
+    // 4 rows per lane when it fits (measured best from 768^2 to 3072^2,
+    // tools/labrd2_rpl_sweep.py), else the geometry with the most CTAs
+    const bool better = !two_phase || (rpl != 4 && (cand == 4 || Gr * Gc > la.Gr * la.Gc));
+    if (bytes <= (size_t)kLabrdSmemMax && better) {
       two_phase = true;
       rpl = cand;
       smem = bytes;
