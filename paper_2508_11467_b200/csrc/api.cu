@@ -25,6 +25,7 @@ extern int g_labrd2_rpl;
 extern double g_labrd_l2keep;
 extern double g_labrd_l2keep_min;
 extern int g_gebd2_cluster;
+extern int g_g2c_max_cols;
 int set_rankk_prefetch(int on);
 int set_rankk_chunk(int c);
 int set_rankk_bulk(int on);
@@ -481,6 +482,12 @@ int dcsvd_debug_rankk_ws(int on) {
 int dcsvd_debug_labrd_variant(void) { return dc::g_labrd_last_two_phase ? 2 : 4; }
 
 /* GEBD2 tail on one thread-block cluster (1, default; 8 = force 8-CTA clusters) or the panel path only (0); debug */
+/* largest trailing block (columns) handed to the cluster GEBD2 kernel (debug / tuning; default 512) */
+int dcsvd_debug_gebd2_max_cols(int n) {
+  dc::g_g2c_max_cols = n > 0 ? n : 512;
+  return 0;
+}
+
 int dcsvd_debug_gebd2_cluster(int on) {
   dc::g_gebd2_cluster = on;
   return 0;

@@ -1248,10 +1248,10 @@ static int gebd2c_cluster_size() {
 // Measured per-column crossover with the two-phase LABRD panels (tools/gebd2_cluster_ab.py):
 // the cluster kernel's work per CTA grows with n^2/16 while the panel path is
 // latency-flat at ~11.5 us per column, so it takes over at n <= 512.
-constexpr int kG2cMaxCols = 512;
+int g_g2c_max_cols = 512;  // debug / tuning: largest trailing block handed to the cluster GEBD2
 
 static bool gebd2c_fits(int m, int n) {
-  if (!g_gebd2_cluster || n < 64 || n > kG2cMaxCols) return false;
+  if (!g_gebd2_cluster || n < 64 || n > g_g2c_max_cols) return false;
   return gebd2c_bytes(m, n, gebd2c_cluster_size(), nullptr, nullptr) <= (size_t)kG2cSmemMax;
 }
 
