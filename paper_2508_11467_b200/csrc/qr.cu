@@ -144,6 +144,19 @@ __global__ void splitk_reduce_kernel(double* __restrict__ Zp, long long count, i
   }
 }
 
+// Split-K reduce for many partials and few outputs (the thin CWY products of
+// the tall QR: 32 x 96 outputs, 74-127 slices): one warp per output, lanes
+// over the slices in fixed order, then a fixed shuffle tree (deterministic).
+__global__ void splitk_reduce_warp_kernel(double* __restrict__ Zp, long long count, int S) {
+  const long long o = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (o >= count) return;
+  double v = 0.0;
+  for (int s = lane; s < S; s += 32) v += Zp[(long long)s * count + o];
+  v = warp_sum(v);
+  if (lane == 0) Zp[o] = v;
+}
+
 static int grid_for(long long n, int threads = 256) {
   long long g = (n + threads - 1) / threads;
   if (g > 148 * 16) g = 148 * 16;
@@ -290,7 +303,10 @@ static int cwy_apply(dcsvd_ctx* h, cudaStream_t st, char side, bool trans, bool 
   }
   const long long zc = (long long)w * c_other;
   if (S > 1) {
-    splitk_reduce_kernel<<<grid_for(zc), 256, 0, st>>>(Zp, zc, S);
+    if (S >= 16 && zc <= (1 << 16))
+      splitk_reduce_warp_kernel<<<(unsigned)((zc * 32 + 255) / 256), 256, 0, st>>>(Zp, zc, S);
+    else
+      splitk_reduce_kernel<<<grid_for(zc), 256, 0, st>>>(Zp, zc, S);
     note_launch();
   }
   // X = op(T) Z  (left, w x c_other) or Z op(T) (right, c_other x w); in place
