@@ -12,6 +12,7 @@
 // inverts it (so the reference's TRSM becomes one small GEMM X = T Z), then
 // C -= Y X.  The unblocked QR panel is a cooperative kernel that keeps each
 // CTA's row slab of the panel in shared memory for all its columns.
+#include <algorithm>
 #include <vector>
 
 #include "ctx.cuh"
@@ -600,6 +601,7 @@ int orgqr_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long nrefl, long 
 // GEMM, kPreGSplit K-slices), Tinv_b and op(T_b) in one launch each before the
 // apply loop, instead of three launches per block on the loop's critical path.
 constexpr int kPreGSplit = 4;
+constexpr size_t kOrmbrPreMaxBytes = size_t(4) << 30;  // resident Y of all blocks (n ~ 32 000)
 int g_ormbr_pre = 1;  // debug: 0 = per-block T inside the apply loop
 
 int ormbr_run(dcsvd_ctx* h, cudaStream_t st, char vect, bool trans, long long m, long long n, const double* A,
@@ -616,16 +618,22 @@ int ormbr_run(dcsvd_ctx* h, cudaStream_t st, char vect, bool trans, long long m,
   const long long c_other = isq ? c_cols : c_rows;
   const long long nblk = (count + nb - 1) / nb;
   if (nblk == 0) return 0;
-  const long long nfull = g_ormbr_pre ? count / nb : 0;     // blocks with precomputed op(T)
   std::vector<long long> yoff(nblk + 1, 0);
   for (long long b = 0; b < nblk; ++b) yoff[b + 1] = yoff[b] + (rows0 - b * nb) * nb;
+  // every block's Y stays resident (n^2/2 doubles per side): above kOrmbrPreMaxBytes
+  // (inputs of tens of GB) the blocks are built one at a time into one buffer
+  // and op(T) is formed per block inside cwy_apply, as before the precompute
+  const bool pre = g_ormbr_pre && (size_t)yoff[nblk] * sizeof(double) <= kOrmbrPreMaxBytes;
+  if (!pre) std::fill(yoff.begin(), yoff.end(), 0LL);
+  const long long ylen = pre ? yoff[nblk] : rows0 * nb;
+  const long long nfull = pre ? count / nb : 0;     // blocks with precomputed op(T)
   const size_t ww = (size_t)nb * nb;
-  const size_t need = pool_bytes((size_t)yoff[nblk], 8) + pool_bytes(cwy_total_scratch(h->sms, rows0, c_other, nb), 8) +
+  const size_t need = pool_bytes((size_t)ylen, 8) + pool_bytes(cwy_total_scratch(h->sms, rows0, c_other, nb), 8) +
                       (nfull ? pool_bytes((size_t)nfull * kPreGSplit * ww, 8) + 2 * pool_bytes((size_t)nfull * ww, 8)
                              : 0);
   int rc = pool_reserve(h, 0, need, st);
   if (rc) return rc;
-  double* Yall = pool_take<double>(h, 0, (size_t)yoff[nblk]);
+  double* Yall = pool_take<double>(h, 0, (size_t)ylen);
   double* scr = pool_take<double>(h, 0, cwy_total_scratch(h->sms, rows0, c_other, nb));
   double* Gall = nfull ? pool_take<double>(h, 0, (size_t)nfull * kPreGSplit * ww) : nullptr;
   double* Tinv = nfull ? pool_take<double>(h, 0, (size_t)nfull * ww) : nullptr;
@@ -633,13 +641,15 @@ int ormbr_run(dcsvd_ctx* h, cudaStream_t st, char vect, bool trans, long long m,
   // Y ('Q': rows x w, ld rows) / Y^T ('P': w x rows, ld w) of every block
   auto block_rows = [&](long long bi) { return rows0 - bi * nb; };
   auto block_w = [&](long long bi) { return (int)std::min<long long>(nb, count - bi * nb); };
-  for (long long bi = 0; bi < nblk; ++bi) {
+  auto build_block_y = [&](long long bi) {
     const long long off = bi * nb, rows = block_rows(bi);
     const int w = block_w(bi);
     const double* src = isq ? A + off + off * lda : A + off + (off + 1) * lda;
     build_y_kernel<<<grid_for(rows * w), 256, 0, st>>>(isq ? 0 : 1, src, lda, tau + off, (int)rows, w, Yall + yoff[bi]);
     note_launch();
-  }
+  };
+  if (pre)
+    for (long long bi = 0; bi < nblk; ++bi) build_block_y(bi);
   if (nfull) {
     for (long long b0 = 0; b0 < nfull; b0 += kMaxBatchDesc) {
       GemmBatch gb;
@@ -672,6 +682,7 @@ int ormbr_run(dcsvd_ctx* h, cudaStream_t st, char vect, bool trans, long long m,
     const long long off = bi * nb, rows = block_rows(bi);
     const int w = block_w(bi);
     const double* utop = bi < nfull ? Top + (size_t)bi * ww : nullptr;
+    if (!pre) build_block_y(bi);  // yoff == 0: the single block buffer
     if (isq)
       rc = cwy_apply(h, st, 'L', trans, false, Yall + yoff[bi], rows, tau + off, w, rows, C + off, ldc, c_cols, scr,
                      nullptr, 0, utop);
