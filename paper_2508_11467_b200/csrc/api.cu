@@ -22,6 +22,7 @@ std::atomic<long long> g_launch_count{0};
 extern unsigned long long* g_labrd_tlog;
 extern int g_labrd_gmax;
 extern int g_labrd2_rpl;
+extern int g_labrd4_rpl;
 extern double g_labrd_l2keep;
 extern double g_labrd_l2keep_min;
 extern int g_gebd2_cluster;
@@ -532,6 +533,11 @@ int dcsvd_debug_ormbr_pre(int on) {
 }
 
 /* force the two-phase LABRD geometry (rows per lane 2/4/8/16; 0 = automatic; debug / tuning) */
+int dcsvd_debug_labrd4_rpl(int rpl) {
+  dc::g_labrd4_rpl = rpl;
+  return 0;
+}
+
 int dcsvd_debug_labrd2_rpl(int rpl) {
   dc::g_labrd2_rpl = rpl;
   return 0;

@@ -1364,6 +1364,7 @@ static int labrd_panel_width(int mv, int nv, int nb, int G) {
 // ldp) and Q (nv x 2nb, ldq) are zeroed here and filled; only the panel
 // rows/columns of Av change.
 int g_labrd_gmax = 0;  // debug: cap on the LABRD grid (0 = all SMs)
+int g_labrd4_rpl = 0;  // debug: rows per lane of the four-phase kernel (0 = square-block heuristic)
 int g_labrd2_rpl = 0;  // debug: rows per lane of the two-phase kernel (0 = the fitting one with most CTAs)
 // bytes of each large-panel GEMV pass kept in L2 with evict_last, the rest evict_first
 // (tools/labrd_l2keep_ab.py at 8192^2: GEBRD 539 -> 532 ms for 16-24 MB; 64+ MB is slower)
@@ -1426,6 +1427,7 @@ static int labrd_launch(dcsvd_ctx* h, cudaStream_t st, int mv, int nv, double* A
     if (target_rows <= 32 * 2) rpl = 2;
     else if (target_rows <= 32 * 4) rpl = 4;
     else if (target_rows <= 32 * 8) rpl = 8;
+    if (g_labrd4_rpl) rpl = g_labrd4_rpl;  // debug: force the four-phase geometry
     int Gr, Gc, CB;
     geom(rpl, Gr, Gc, CB);
     if (Gr > G) return set_error(h, DCSVD_EINVAL, "matrix too tall for the GPU LABRD panel (%d rows)", mv);
