@@ -215,6 +215,45 @@ def test_gebrd_halfwidth_panels(cuda):
     assert np.max(np.abs(out[1][2] - out[0][2])) <= SIG_TOL * 3072 * out[0][2][0]
 
 
+def test_ormbr_batched_t_matches_per_block(cuda):
+    """ORMBR with op(T) of all full CWY blocks precomputed in batched launches
+    (qr.cu ormbr_run) gives the per-block result up to rounding: 700^2 has five
+    full 128-wide blocks per side plus a partial one."""
+    g = _g()
+    lib = _lib_handle()
+    a = g.generate_matrix(g.MatrixSpec("random", 700, 700, seed=4), device=True)
+    out = {}
+    try:
+        for pre in (0, 1):
+            lib.dcsvd_debug_ormbr_pre(pre)
+            r = g.gesdd(a)
+            out[pre] = (r.sigma.clone(), r.u.clone(), r.vt.clone())
+    finally:
+        lib.dcsvd_debug_ormbr_pre(1)
+    assert torch.equal(out[0][0], out[1][0])  # sigma does not depend on the back-transform
+    assert float((out[0][1] - out[1][1]).abs().max()) <= 1e-13
+    assert float((out[0][2] - out[1][2]).abs().max()) <= 1e-13
+
+
+@pytest.mark.parametrize("rpl", [2, 4, 8])
+def test_labrd2_geometries_agree(cuda, rpl):
+    """The two-phase LABRD kernel gives the same bidiagonal for every block
+    geometry it can take (rows per lane forced through the debug knob; the
+    default prefers 4), within rounding of the different reduction trees."""
+    g = _g()
+    lib = _lib_handle()
+    a = g.generate_matrix(g.MatrixSpec("random", 1536, 1400, seed=6), device=True)
+    ref = g.gebrd_blocked(a.clone())
+    try:
+        lib.dcsvd_debug_labrd2_rpl(rpl)
+        f = g.gebrd_blocked(a.clone())
+    finally:
+        lib.dcsvd_debug_labrd2_rpl(0)
+    sc = float(torch.linalg.norm(a))
+    assert float((f.d.abs() - ref.d.abs()).abs().max()) <= 1e-12 * sc
+    assert float((f.e.abs() - ref.e.abs()).abs().max()) <= 1e-12 * sc
+
+
 def test_gebrd_unblocked_and_panel(cuda):
     g = _g()
     rng = np.random.default_rng(6)
