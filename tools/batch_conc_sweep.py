@@ -9,7 +9,7 @@ import paper_2508_11467_b200 as g
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
 batch = int(sys.argv[2]) if len(sys.argv) > 2 else 16
 mats = [torch.rand(n, n, dtype=torch.float64, device="cuda").t() for _ in range(batch)]
-for conc in (2, 4, 6, 8, 12, 16):
+for conc in [int(x) for x in os.environ.get("CONCS", "2 4 6 8 12 16").split()]:
     g.gesdd_batched(mats, concurrency=conc)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
