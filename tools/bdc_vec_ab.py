@@ -1,0 +1,25 @@
+"""BDC middle-matrix vectors: CTA-per-column staged kernel vs warp-per-column
+(dcsvd_debug_bdc_vec_cta): gesdd time, BDC phase, U/Vt agreement."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2508_11467_b200 as g
+from paper_2508_11467_b200 import _lib
+lib = _lib.load_library()
+for n in [int(x) for x in sys.argv[1:]] or [2048, 8192]:
+    a = g.generate_matrix(g.MatrixSpec("random", n, n, seed=2), device=True)
+    res = {}
+    for on in (0, 1):
+        lib.dcsvd_debug_bdc_vec_cta(on)
+        r = g.gesdd(a); torch.cuda.synchronize()
+        ts = []
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(); g.gesdd(a); e1.record(); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
+        bdc = [t for k, t in g.phase_profile(a).phases if k == "bdcdc"][0]
+        res[on] = (r, min(ts), bdc * 1e3)
+    r0, r1 = res[0][0], res[1][0]
+    print(f"n {n}: warp {res[0][1]:.2f} ms (BDC {res[0][2]:.2f}) cta {res[1][1]:.2f} ms (BDC {res[1][2]:.2f}) | "
+          f"dsigma {float((r0.sigma - r1.sigma).abs().max()):.1e} dU {float((r0.u - r1.u).abs().max()):.1e} "
+          f"dVt {float((r0.vt - r1.vt).abs().max()):.1e}", flush=True)
+lib.dcsvd_debug_bdc_vec_cta(1)
