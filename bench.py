@@ -655,7 +655,7 @@ def main():
         "frac": (achieved / hbm) if achieved else None,
         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
         "traffic": ncu.get("labrd_dram_bytes_per_step") if args.workload == "c2" else None,
-        "traffic_note": ("DRAM bytes per step = sum of dram__bytes_read + dram__bytes_write over all 241 LABRD/GEBD2 "
+        "traffic_note": ("DRAM bytes per step = sum of dram__bytes_read + dram__bytes_write over all 300 LABRD/GEBD2 "
                          "launches of one 8192^2 GEBRD (ncu --cache-control none, profiles/labrd_dram_r02.csv, "
                          "profiles/ncu_r02_labrd_dram.md): 65 % of the algorithmic bytes -- the snake order and L2 "
                          "hints serve the rest from L2") if args.workload == "c2" else "C2 capture only",
