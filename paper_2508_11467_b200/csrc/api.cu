@@ -44,6 +44,7 @@ extern int g_cwy_split_mode;
 extern int g_cwy_gsplit;
 extern int g_qr_outer;
 int g_ts_qr_nb = 0;   // debug: QR panel width of the TS pre-step (0 = options.qr_block)
+int g_ormbr_overlap = 1;  // debug: 0 = ORMBR preparation after BDC (no overlap)
 int g_ts_literal = 1;  // TS recombination: 1 = ORGQR + GEMM (driver.py:141-142), 0 = fused reflector apply
 int set_ws_flags(int f);
 thread_local dcsvd_ctx* t_cur = nullptr;
@@ -263,7 +264,8 @@ static dcsvd_ctx* side_ctx(dcsvd_ctx* h) {
     h->side = make_sub(h, h->sms);
     if (!h->side) return nullptr;
     if (cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_prep, cudaEventDisableTiming) != cudaSuccess)
       return nullptr;
   }
   h->side->stats_on = h->stats_on;
@@ -283,37 +285,66 @@ int square_core(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double*
   pt.mark(PH_GEBRD);
   int rc = gebrd_run(h, st, m, n, A, lda, d, e, tq, tp, o.bidiag_block);
   if (rc) return rc;
-  pt.mark(PH_BDC);
   const bool vec = o.want_vectors != 0;
+  // The U and V^T back-transforms are independent: on a whole-GPU handle the
+  // V^T one runs on a side stream with its own workspace, so the small
+  // kernels and wave tails of one fill the other's gaps.  Their preparation
+  // (every CWY block's Y and op(T), qr.cu ormbr_prepare) needs only the
+  // packed reflectors, so the side stream does it for both sides while BDC
+  // runs on `st` (BDC uses pool 2 only; the U plan lives in pool 0 of h).
+  dcsvd_ctx* sd = vec ? side_ctx(h) : nullptr;
+  OrmbrPlan planU, planV;
+  const bool overlap = sd && g_ormbr_overlap;
+  auto join_side = [&]() {
+    h->last_error = sd->last_error;
+    cudaStreamSynchronize(sd->own_stream);
+  };
+  if (overlap) {
+    DC_CUDA_TRY(cudaEventRecord(h->ev_fork, st));
+    DC_CUDA_TRY(cudaStreamWaitEvent(sd->own_stream, h->ev_fork, 0));
+    rc = ormbr_prepare(sd, sd->own_stream, 'P', true, m, n, A, lda, tp, n, n, kDriverCwyWidth, planV);
+    if (!rc) rc = ormbr_prepare(h, sd->own_stream, 'Q', false, m, n, A, lda, tq, m, n, kDriverCwyWidth, planU);
+    if (rc) {
+      if (h->last_error.empty()) h->last_error = sd->last_error;
+      cudaStreamSynchronize(sd->own_stream);
+      return rc;
+    }
+    DC_CUDA_TRY(cudaEventRecord(h->ev_prep, sd->own_stream));
+  }
+  pt.mark(PH_BDC);
   rc = bdsdc_run(h, st, n, d, e, false, vec, o.leaf_size, o.deflation_multiple, S, nullptr, vec ? U : nullptr, ldu,
                  m, nullptr, 0, vec ? VT : nullptr, ldvt);
-  if (rc) return rc;
+  if (rc) {
+    if (overlap) cudaStreamSynchronize(sd->own_stream);
+    return rc;
+  }
   if (!vec) return 0;
   pt.mark(PH_ORMBR);
   // The driver groups reflectors into the widest CWY panels the GPU kernels
   // take (kDriverCwyWidth): T^-1 = triu(Y^T Y) + diag(1/tau) is exact for any
   // width, so this is the same product as the reference's 64-wide blocks
   // (backtransform.py:90-131) with fewer, larger DMMA GEMMs.
-  // The U and V^T back-transforms are independent: on a whole-GPU handle the
-  // V^T one runs on a side stream with its own workspace, so the small
-  // kernels and wave tails of one fill the other's gaps.
-  dcsvd_ctx* sd = side_ctx(h);
   if (!sd) {
     rc = ormbr_run(h, st, 'Q', false, m, n, A, lda, tq, U, m, n, ldu, kDriverCwyWidth);
     if (rc) return rc;
     return ormbr_run(h, st, 'P', true, m, n, A, lda, tp, VT, n, n, ldvt, kDriverCwyWidth);
   }
-  DC_CUDA_TRY(cudaEventRecord(h->ev_fork, st));
+  DC_CUDA_TRY(cudaEventRecord(h->ev_fork, st));  // BDC done (U, V^T initialised)
   DC_CUDA_TRY(cudaStreamWaitEvent(sd->own_stream, h->ev_fork, 0));
-  rc = ormbr_run(sd, sd->own_stream, 'P', true, m, n, A, lda, tp, VT, n, n, ldvt, kDriverCwyWidth);
+  rc = overlap ? ormbr_apply(sd, sd->own_stream, planV, VT, ldvt)
+               : ormbr_run(sd, sd->own_stream, 'P', true, m, n, A, lda, tp, VT, n, n, ldvt, kDriverCwyWidth);
   if (rc) {
     // join the side stream before reporting: its enqueued kernels may still
     // read A / tp and write VT, which the caller frees after an error
-    h->last_error = sd->last_error;
-    cudaStreamSynchronize(sd->own_stream);
+    join_side();
     return rc;
   }
-  rc = ormbr_run(h, st, 'Q', false, m, n, A, lda, tq, U, m, n, ldu, kDriverCwyWidth);
+  if (overlap) {
+    DC_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_prep, 0));
+    rc = planU.nblk ? ormbr_apply(h, st, planU, U, ldu) : 0;
+  } else {
+    rc = ormbr_run(h, st, 'Q', false, m, n, A, lda, tq, U, m, n, ldu, kDriverCwyWidth);
+  }
   DC_CUDA_TRY(cudaEventRecord(h->ev_join, sd->own_stream));
   DC_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_join, 0));
   merge_err_kernel<<<1, 1, 0, st>>>(h->d_err, sd->d_err);
@@ -523,6 +554,12 @@ int dcsvd_debug_labrd_l2keep_min(double bytes) {
 int dcsvd_debug_labrd_halfwidth(int on, long long max_elems) {
   dc::g_labrd_halfwidth = on;
   dc::g_labrd_halfwidth_max = max_elems > 0 ? max_elems : (1LL << 62);
+  return 0;
+}
+
+/* ORMBR preparation on the side stream during BDC (1, default) or after it (0); debug */
+int dcsvd_debug_ormbr_overlap(int on) {
+  dc::g_ormbr_overlap = on;
   return 0;
 }
 
@@ -802,6 +839,7 @@ static void free_ctx_resources(dcsvd_ctx* h) {
     h->side = nullptr;
     cudaEventDestroy(h->ev_fork);
     cudaEventDestroy(h->ev_join);
+    if (h->ev_prep) cudaEventDestroy(h->ev_prep);
   }
   for (auto& p : h->pool)
     if (p.ptr) cudaFree(p.ptr);

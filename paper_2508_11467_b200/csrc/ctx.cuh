@@ -18,6 +18,7 @@ struct dcsvd_ctx {
   dcsvd_ctx* side = nullptr;    // second stream + workspace for independent stages (V^T back-transform)
   bool is_sub = false;          // batch / side sub-context (no further splitting)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // side-stream fork/join
+  cudaEvent_t ev_prep = nullptr;  // side stream: ORMBR preparation done
   cudaStream_t own_stream = nullptr;
   int device = 0;
   int sms = 148;
@@ -85,6 +86,22 @@ int orgqr_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long nrefl, long 
 // Left apply of column reflectors stored below the diagonal of A (rows >= j of
 // reflector j, offset `roff` = 0) or right apply of row reflectors stored right
 // of the superdiagonal (offset 1).  See qr.cu.
+// ORMBR in two steps (qr.cu): the prepare step (pool 0 of h, every block's Y,
+// batched op(T)) reads only the packed reflectors; apply runs the block loop.
+struct OrmbrPlan {
+  bool isq = true, trans = false, pre = false;
+  int nb = 0;
+  const double* A = nullptr;
+  long long lda = 0;
+  const double* tau = nullptr;
+  long long c_rows = 0, c_cols = 0, count = 0, rows0 = 0, nblk = 0, nfull = 0;
+  std::vector<long long> yoff;
+  double *Yall = nullptr, *scr = nullptr, *Top = nullptr;
+};
+int ormbr_prepare(dcsvd_ctx* h, cudaStream_t st, char vect, bool trans, long long m, long long n, const double* A,
+                  long long lda, const double* tau, long long c_rows, long long c_cols, int nb, OrmbrPlan& P);
+void ormbr_build_y(cudaStream_t st, const OrmbrPlan& P, long long bi);
+int ormbr_apply(dcsvd_ctx* h, cudaStream_t st, const OrmbrPlan& P, double* C, long long ldc);
 int ormbr_run(dcsvd_ctx* h, cudaStream_t st, char vect, bool trans, long long m, long long n,
               const double* A, long long lda, const double* tau, double* C, long long c_rows,
               long long c_cols, long long ldc, int nb);

@@ -604,95 +604,117 @@ constexpr int kPreGSplit = 4;
 constexpr size_t kOrmbrPreMaxBytes = size_t(4) << 30;  // resident Y of all blocks (n ~ 32 000)
 int g_ormbr_pre = 1;  // debug: 0 = per-block T inside the apply loop
 
-int ormbr_run(dcsvd_ctx* h, cudaStream_t st, char vect, bool trans, long long m, long long n, const double* A,
-              long long lda, const double* tau, double* C, long long c_rows, long long c_cols, long long ldc,
-              int nb) {
+// ormbr_run = ormbr_prepare (pool, Y of every block, batched op(T); depends only
+// on the packed reflectors) + ormbr_apply (the block loop on C).  The driver
+// runs the prepare step of both sides on a side stream while BDC runs.
+int ormbr_prepare(dcsvd_ctx* h, cudaStream_t st, char vect, bool trans, long long m, long long n, const double* A,
+                  long long lda, const double* tau, long long c_rows, long long c_cols, int nb, OrmbrPlan& P) {
   if (nb < 1) return set_error(h, DCSVD_EINVAL, "block width must be >= 1, got %d", nb);
   if (nb > kCwyMaxW) nb = kCwyMaxW;  // same product, grouped in 128-wide compact-WY blocks
   if (vect != 'Q' && vect != 'P') return set_error(h, DCSVD_EINVAL, "vect must be 'Q' or 'P'");
   const bool isq = vect == 'Q';
   if (isq && c_rows != m) return set_error(h, DCSVD_EINVAL, "C has %lld rows, sequence acts on %lld", c_rows, m);
   if (!isq && c_cols != n) return set_error(h, DCSVD_EINVAL, "C has %lld columns, sequence acts on %lld", c_cols, n);
-  const long long count = isq ? n : (n > 0 ? n - 1 : 0);  // reflectors
-  const long long rows0 = isq ? m : n - 1;                 // rows of block 0's reflectors
+  P = OrmbrPlan();
+  P.isq = isq; P.trans = trans; P.nb = nb; P.A = A; P.lda = lda; P.tau = tau;
+  P.c_rows = c_rows; P.c_cols = c_cols;
+  P.count = isq ? n : (n > 0 ? n - 1 : 0);  // reflectors
+  P.rows0 = isq ? m : n - 1;                 // rows of block 0's reflectors
   const long long c_other = isq ? c_cols : c_rows;
-  const long long nblk = (count + nb - 1) / nb;
-  if (nblk == 0) return 0;
-  std::vector<long long> yoff(nblk + 1, 0);
-  for (long long b = 0; b < nblk; ++b) yoff[b + 1] = yoff[b] + (rows0 - b * nb) * nb;
+  P.nblk = (P.count + nb - 1) / nb;
+  if (P.nblk == 0) return 0;
+  P.yoff.assign(P.nblk + 1, 0);
+  for (long long b = 0; b < P.nblk; ++b) P.yoff[b + 1] = P.yoff[b] + (P.rows0 - b * nb) * nb;
   // every block's Y stays resident (n^2/2 doubles per side): above kOrmbrPreMaxBytes
   // (inputs of tens of GB) the blocks are built one at a time into one buffer
   // and op(T) is formed per block inside cwy_apply, as before the precompute
-  const bool pre = g_ormbr_pre && (size_t)yoff[nblk] * sizeof(double) <= kOrmbrPreMaxBytes;
-  if (!pre) std::fill(yoff.begin(), yoff.end(), 0LL);
-  const long long ylen = pre ? yoff[nblk] : rows0 * nb;
-  const long long nfull = pre ? count / nb : 0;     // blocks with precomputed op(T)
+  P.pre = g_ormbr_pre && (size_t)P.yoff[P.nblk] * sizeof(double) <= kOrmbrPreMaxBytes;
+  if (!P.pre) std::fill(P.yoff.begin(), P.yoff.end(), 0LL);
+  const long long ylen = P.pre ? P.yoff[P.nblk] : P.rows0 * nb;
+  P.nfull = P.pre ? P.count / nb : 0;  // blocks with precomputed op(T)
   const size_t ww = (size_t)nb * nb;
-  const size_t need = pool_bytes((size_t)ylen, 8) + pool_bytes(cwy_total_scratch(h->sms, rows0, c_other, nb), 8) +
-                      (nfull ? pool_bytes((size_t)nfull * kPreGSplit * ww, 8) + 2 * pool_bytes((size_t)nfull * ww, 8)
-                             : 0);
+  const size_t need = pool_bytes((size_t)ylen, 8) + pool_bytes(cwy_total_scratch(h->sms, P.rows0, c_other, nb), 8) +
+                      (P.nfull ? pool_bytes((size_t)P.nfull * kPreGSplit * ww, 8) + 2 * pool_bytes((size_t)P.nfull * ww, 8)
+                               : 0);
   int rc = pool_reserve(h, 0, need, st);
   if (rc) return rc;
-  double* Yall = pool_take<double>(h, 0, (size_t)ylen);
-  double* scr = pool_take<double>(h, 0, cwy_total_scratch(h->sms, rows0, c_other, nb));
-  double* Gall = nfull ? pool_take<double>(h, 0, (size_t)nfull * kPreGSplit * ww) : nullptr;
-  double* Tinv = nfull ? pool_take<double>(h, 0, (size_t)nfull * ww) : nullptr;
-  double* Top = nfull ? pool_take<double>(h, 0, (size_t)nfull * ww) : nullptr;
-  // Y ('Q': rows x w, ld rows) / Y^T ('P': w x rows, ld w) of every block
-  auto block_rows = [&](long long bi) { return rows0 - bi * nb; };
-  auto block_w = [&](long long bi) { return (int)std::min<long long>(nb, count - bi * nb); };
-  auto build_block_y = [&](long long bi) {
-    const long long off = bi * nb, rows = block_rows(bi);
-    const int w = block_w(bi);
-    const double* src = isq ? A + off + off * lda : A + off + (off + 1) * lda;
-    build_y_kernel<<<grid_for(rows * w), 256, 0, st>>>(isq ? 0 : 1, src, lda, tau + off, (int)rows, w, Yall + yoff[bi]);
-    note_launch();
-  };
-  if (pre)
-    for (long long bi = 0; bi < nblk; ++bi) build_block_y(bi);
-  if (nfull) {
-    for (long long b0 = 0; b0 < nfull; b0 += kMaxBatchDesc) {
+  P.Yall = pool_take<double>(h, 0, (size_t)ylen);
+  P.scr = pool_take<double>(h, 0, cwy_total_scratch(h->sms, P.rows0, c_other, nb));
+  double* Gall = P.nfull ? pool_take<double>(h, 0, (size_t)P.nfull * kPreGSplit * ww) : nullptr;
+  double* Tinv = P.nfull ? pool_take<double>(h, 0, (size_t)P.nfull * ww) : nullptr;
+  P.Top = P.nfull ? pool_take<double>(h, 0, (size_t)P.nfull * ww) : nullptr;
+  if (!P.pre) return 0;
+  for (long long bi = 0; bi < P.nblk; ++bi) ormbr_build_y(st, P, bi);
+  if (P.nfull) {
+    for (long long b0 = 0; b0 < P.nfull; b0 += kMaxBatchDesc) {
       GemmBatch gb;
-      gb.count = (int)std::min<long long>(kMaxBatchDesc, nfull - b0);
+      gb.count = (int)std::min<long long>(kMaxBatchDesc, P.nfull - b0);
       gb.ksplit = kPreGSplit;
-      gb.kchunk = (int)((((block_rows(b0) + kPreGSplit - 1) / kPreGSplit) + 15) & ~15LL);
+      gb.kchunk = (int)((((P.rows0 - b0 * nb + kPreGSplit - 1) / kPreGSplit) + 15) & ~15LL);
       gb.cslice = (long long)ww;
       for (int i = 0; i < gb.count; ++i) {
         const long long bi = b0 + i;
+        const long long rows = P.rows0 - bi * nb;
         GemmDesc g;
         g.acol = nullptr; g.ccol = nullptr; g.alpha = 1.0; g.beta = 0.0;
-        g.m = nb; g.n = nb; g.k = (int)block_rows(bi);
-        g.A = Yall + yoff[bi]; g.B = Yall + yoff[bi];
-        g.lda = g.ldb = isq ? block_rows(bi) : nb;
+        g.m = nb; g.n = nb; g.k = (int)rows;
+        g.A = P.Yall + P.yoff[bi]; g.B = P.Yall + P.yoff[bi];
+        g.lda = g.ldb = isq ? rows : nb;
         g.C = Gall + (size_t)bi * kPreGSplit * ww; g.ldc = nb;
         gb.d[i] = g;
       }
       rc = isq ? gemm_launch_batch(st, true, false, gb) : gemm_launch_batch(st, false, true, gb);
       if (rc) return rc;
     }
-    cwy_tinv_build_kernel<<<dim3((unsigned)((ww + 255) / 256), (unsigned)nfull), 256, 0, st>>>(
+    cwy_tinv_build_kernel<<<dim3((unsigned)((ww + 255) / 256), (unsigned)P.nfull), 256, 0, st>>>(
         Gall, kPreGSplit, nb, tau, Tinv, h->d_err, (long long)kPreGSplit * ww, nb);
     note_launch();
-    rc = tinv_solve_launch(st, Tinv, nb, trans, Top, (int)nfull);
-    if (rc) return rc;
-  }
-  for (long long b = 0; b < nblk; ++b) {
-    // 'Q': U1^T front-to-back, U1 back-to-front; 'P': V1^T back-to-front, V1 front-to-back
-    const long long bi = (isq == trans) ? b : nblk - 1 - b;
-    const long long off = bi * nb, rows = block_rows(bi);
-    const int w = block_w(bi);
-    const double* utop = bi < nfull ? Top + (size_t)bi * ww : nullptr;
-    if (!pre) build_block_y(bi);  // yoff == 0: the single block buffer
-    if (isq)
-      rc = cwy_apply(h, st, 'L', trans, false, Yall + yoff[bi], rows, tau + off, w, rows, C + off, ldc, c_cols, scr,
-                     nullptr, 0, utop);
-    else
-      rc = cwy_apply(h, st, 'R', trans, true, Yall + yoff[bi], w, tau + off, w, rows, C + (off + 1) * ldc, ldc, c_rows,
-                     scr, nullptr, 0, utop);
+    rc = tinv_solve_launch(st, Tinv, nb, trans, P.Top, (int)P.nfull);
     if (rc) return rc;
   }
   DC_CUDA_TRY(cudaGetLastError());
   return 0;
+}
+
+void ormbr_build_y(cudaStream_t st, const OrmbrPlan& P, long long bi) {
+  const long long off = bi * P.nb, rows = P.rows0 - bi * P.nb;
+  const int w = (int)std::min<long long>(P.nb, P.count - off);
+  const double* src = P.isq ? P.A + off + off * P.lda : P.A + off + (off + 1) * P.lda;
+  build_y_kernel<<<grid_for(rows * w), 256, 0, st>>>(P.isq ? 0 : 1, src, P.lda, P.tau + off, (int)rows, w,
+                                                    P.Yall + P.yoff[bi]);
+  note_launch();
+}
+
+int ormbr_apply(dcsvd_ctx* h, cudaStream_t st, const OrmbrPlan& P, double* C, long long ldc) {
+  const int nb = P.nb;
+  const size_t ww = (size_t)nb * nb;
+  int rc = 0;
+  for (long long b = 0; b < P.nblk; ++b) {
+    // 'Q': U1^T front-to-back, U1 back-to-front; 'P': V1^T back-to-front, V1 front-to-back
+    const long long bi = (P.isq == P.trans) ? b : P.nblk - 1 - b;
+    const long long off = bi * nb, rows = P.rows0 - bi * nb;
+    const int w = (int)std::min<long long>(nb, P.count - off);
+    const double* utop = bi < P.nfull ? P.Top + (size_t)bi * ww : nullptr;
+    if (!P.pre) ormbr_build_y(st, P, bi);  // yoff == 0: the single block buffer
+    if (P.isq)
+      rc = cwy_apply(h, st, 'L', P.trans, false, P.Yall + P.yoff[bi], rows, P.tau + off, w, rows, C + off, ldc,
+                     P.c_cols, P.scr, nullptr, 0, utop);
+    else
+      rc = cwy_apply(h, st, 'R', P.trans, true, P.Yall + P.yoff[bi], w, P.tau + off, w, rows, C + (off + 1) * ldc,
+                     ldc, P.c_rows, P.scr, nullptr, 0, utop);
+    if (rc) return rc;
+  }
+  DC_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int ormbr_run(dcsvd_ctx* h, cudaStream_t st, char vect, bool trans, long long m, long long n, const double* A,
+              long long lda, const double* tau, double* C, long long c_rows, long long c_cols, long long ldc,
+              int nb) {
+  OrmbrPlan P;
+  int rc = ormbr_prepare(h, st, vect, trans, m, n, A, lda, tau, c_rows, c_cols, nb, P);
+  if (rc || P.nblk == 0) return rc;
+  return ormbr_apply(h, st, P, C, ldc);
 }
 
 // ---------------------------------------------------------------------------
