@@ -6,6 +6,7 @@
 #include <stdio.h>
 
 #include <algorithm>
+#include <functional>
 #include <atomic>
 #include <mutex>
 #include <thread>
@@ -45,6 +46,7 @@ extern int g_cwy_gsplit;
 extern int g_qr_outer;
 int g_ts_qr_nb = 0;   // debug: QR panel width of the TS pre-step (0 = options.qr_block)
 int g_ormbr_overlap = 1;  // debug: 0 = ORMBR preparation after BDC (no overlap)
+int g_ts_orgqr_overlap = 1;  // debug: 0 = TS-path ORGQR after the core SVD of R on the call's stream
 int g_ts_literal = 1;  // TS recombination: 1 = ORGQR + GEMM (driver.py:141-142), 0 = fused reflector apply
 int set_ws_flags(int f);
 thread_local dcsvd_ctx* t_cur = nullptr;
@@ -271,13 +273,27 @@ static dcsvd_ctx* side_ctx(dcsvd_ctx* h) {
   h->side->stats_on = h->stats_on;
   return h->side;
 }
+// Second lazily created side context (TS path: ORGQR of the tall QR runs on it
+// while the core SVD of R does its BDC and back-transforms).
+static dcsvd_ctx* side2_ctx(dcsvd_ctx* h) {
+  if (h->is_sub) return nullptr;
+  if (!h->side2) {
+    h->side2 = make_sub(h, h->sms);
+    if (!h->side2) return nullptr;
+    if (cudaEventCreateWithFlags(&h->ev_fork2, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_join2, cudaEventDisableTiming) != cudaSuccess)
+      return nullptr;
+  }
+  h->side2->stats_on = h->stats_on;
+  return h->side2;
+}
 constexpr int kDriverCwyWidth = 128;
 enum { PH_GEQRF = 0, PH_ORGQR, PH_GEBRD, PH_BDC, PH_ORMBR, PH_GEMM, PH_END = -1 };
 
 // _square_core (driver.py:97-118) for m >= n.  A consumed.
 int square_core(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A, long long lda, double* S,
                 double* U, long long ldu, double* VT, long long ldvt, const dcsvd_opts& o, PhaseTimer& pt,
-                double* dbuf) {
+                double* dbuf, const std::function<int()>* after_gebrd = nullptr) {
   double* d = dbuf;
   double* e = d + n;
   double* tq = e + n;
@@ -285,6 +301,10 @@ int square_core(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double*
   pt.mark(PH_GEBRD);
   int rc = gebrd_run(h, st, m, n, A, lda, d, e, tq, tp, o.bidiag_block);
   if (rc) return rc;
+  if (after_gebrd) {  // caller's independent work forked here (gesdd_tall: ORGQR on a third stream)
+    rc = (*after_gebrd)();
+    if (rc) return rc;
+  }
   const bool vec = o.want_vectors != 0;
   // The U and V^T back-transforms are independent: on a whole-GPU handle the
   // V^T one runs on a side stream with its own workspace, so the small
@@ -377,11 +397,38 @@ int gesdd_tall(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* 
     // Q = orgqr(QR, n) (m x n, 128-wide CWY blocks); U = Q U0 (one DMMA GEMM)
     double* U0 = pool_take<double>(h, 1, (size_t)n * n);
     double* Qw = pool_take<double>(h, 1, (size_t)m * n);
-    rc = square_core(h, st, n, n, R, n, S, U0, n, VT, ldvt, o, pt, dbuf);
-    if (rc) return rc;
+    // ORGQR needs only the QR reflectors: outside phase profiling it runs on a
+    // third stream (own workspace) once the cooperative GEBRD of R is done, beside
+    // R's BDC and back-transforms; phase_profile keeps the sequential order so
+    // every PHASE_NAMES phase is timed on the call's stream.
+    dcsvd_ctx* s2 = (!pt.on && g_ts_orgqr_overlap) ? side2_ctx(h) : nullptr;
+    bool forked = false;
+    const std::function<int()> fork_orgqr = [&]() -> int {
+      DC_CUDA_TRY(cudaEventRecord(h->ev_fork2, st));
+      DC_CUDA_TRY(cudaStreamWaitEvent(s2->own_stream, h->ev_fork2, 0));
+      forked = true;
+      const int r2 = orgqr_run(s2, s2->own_stream, m, n, n, A, lda, tau, Qw, m, kDriverCwyWidth);
+      if (r2) {
+        h->last_error = s2->last_error;
+        return r2;
+      }
+      DC_CUDA_TRY(cudaEventRecord(h->ev_join2, s2->own_stream));
+      return 0;
+    };
+    rc = square_core(h, st, n, n, R, n, S, U0, n, VT, ldvt, o, pt, dbuf, s2 ? &fork_orgqr : nullptr);
+    if (rc) {
+      if (forked) cudaStreamSynchronize(s2->own_stream);  // its kernels read A / tau and write Qw
+      return rc;
+    }
     pt.mark(PH_ORGQR);
-    rc = orgqr_run(h, st, m, n, n, A, lda, tau, Qw, m, kDriverCwyWidth);
-    if (rc) return rc;
+    if (s2) {
+      DC_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_join2, 0));
+      merge_err_kernel<<<1, 1, 0, st>>>(h->d_err, s2->d_err);
+      note_launch();
+    } else {
+      rc = orgqr_run(h, st, m, n, n, A, lda, tau, Qw, m, kDriverCwyWidth);
+      if (rc) return rc;
+    }
     pt.mark(PH_GEMM);
     GemmDesc gd{(int)m, (int)n, (int)n, Qw, m, nullptr, U0, n, U, ldu, nullptr, 1.0, 0.0};
     return gemm_launch(st, false, false, gd);
@@ -557,6 +604,12 @@ int dcsvd_debug_labrd_halfwidth(int on, long long max_elems) {
   return 0;
 }
 
+/* TS path: ORGQR on a third stream beside the core SVD of R (1, default) or after it (0); debug */
+int dcsvd_debug_ts_orgqr_overlap(int on) {
+  dc::g_ts_orgqr_overlap = on;
+  return 0;
+}
+
 /* ORMBR preparation on the side stream during BDC (1, default) or after it (0); debug */
 int dcsvd_debug_ormbr_overlap(int on) {
   dc::g_ormbr_overlap = on;
@@ -641,6 +694,7 @@ int dcsvd_set_stats(dcsvd_handle h, int enable) {
   cudaEventSynchronize(h->ev_stats0);
   for (auto* sub : h->subs) dcsvd_set_stats(sub, enable);  // batched sub-contexts record too
   if (h->side) dcsvd_set_stats(h->side, enable);
+  if (h->side2) dcsvd_set_stats(h->side2, enable);
   return 0;
 }
 
@@ -684,6 +738,7 @@ static void collect_stats(dcsvd_ctx* h, cudaEvent_t origin, int kind, std::vecto
   }
   for (auto* sub : h->subs) collect_stats(sub, origin, kind, iv, work, count);
   if (h->side) collect_stats(h->side, origin, kind, iv, work, count);
+  if (h->side2) collect_stats(h->side2, origin, kind, iv, work, count);
 }
 
 int dcsvd_get_stats(dcsvd_handle h, int kind, double* ms, double* work, long long* launches) {
@@ -840,6 +895,13 @@ static void free_ctx_resources(dcsvd_ctx* h) {
     cudaEventDestroy(h->ev_fork);
     cudaEventDestroy(h->ev_join);
     if (h->ev_prep) cudaEventDestroy(h->ev_prep);
+  }
+  if (h->side2) {
+    free_ctx_resources(h->side2);
+    delete h->side2;
+    h->side2 = nullptr;
+    if (h->ev_fork2) cudaEventDestroy(h->ev_fork2);
+    if (h->ev_join2) cudaEventDestroy(h->ev_join2);
   }
   for (auto& p : h->pool)
     if (p.ptr) cudaFree(p.ptr);

@@ -19,6 +19,8 @@ struct dcsvd_ctx {
   bool is_sub = false;          // batch / side sub-context (no further splitting)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // side-stream fork/join
   cudaEvent_t ev_prep = nullptr;  // side stream: ORMBR preparation done
+  dcsvd_ctx* side2 = nullptr;     // third stream + workspace (TS path: ORGQR beside the core SVD of R)
+  cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   cudaStream_t own_stream = nullptr;
   int device = 0;
   int sms = 148;
