@@ -22,6 +22,7 @@ namespace dc {
 std::atomic<long long> g_launch_count{0};
 extern unsigned long long* g_labrd_tlog;
 extern int g_labrd_gmax;
+extern int g_labrd_skip_zero;
 extern int g_labrd2_rpl;
 extern int g_labrd4_rpl;
 extern double g_labrd_l2keep;
@@ -630,6 +631,12 @@ int dcsvd_debug_labrd4_rpl(int rpl) {
 
 int dcsvd_debug_labrd2_rpl(int rpl) {
   dc::g_labrd2_rpl = rpl;
+  return 0;
+}
+
+/* GEBRD panels skip the P / Q zero fill (1, default) or zero them like labrd_panel (0); debug */
+int dcsvd_debug_labrd_skip_zero(int on) {
+  dc::g_labrd_skip_zero = on;
   return 0;
 }
 

@@ -1364,6 +1364,7 @@ static int labrd_panel_width(int mv, int nv, int nb, int G) {
 // ldp) and Q (nv x 2nb, ldq) are zeroed here and filled; only the panel
 // rows/columns of Av change.
 int g_labrd_gmax = 0;  // debug: cap on the LABRD grid (0 = all SMs)
+int g_labrd_skip_zero = 1;  // debug: 0 = zero P / Q before every GEBRD panel as well
 int g_labrd4_rpl = 0;  // debug: rows per lane of the four-phase kernel (0 = square-block heuristic)
 int g_labrd2_rpl = 0;  // debug: rows per lane of the two-phase kernel (0 = the fitting one with most CTAs)
 // bytes of each large-panel GEMV pass kept in L2 with evict_last, the rest evict_first
@@ -1373,10 +1374,15 @@ double g_labrd_l2keep_min = 160.0 * (1 << 20);  // panels whose matrix is smalle
 
 static int labrd_launch(dcsvd_ctx* h, cudaStream_t st, int mv, int nv, double* Av, long long lda, int nb, double* d,
                         double* e, double* tauq, double* taup, double* P, long long ldp, double* Q, long long ldq,
-                        const LabrdWork& w) {
+                        const LabrdWork& w, bool zero_pq = true) {
   const int G = g_labrd_gmax > 0 ? std::min(h->sms, g_labrd_gmax) : h->sms;
-  DC_CUDA_TRY(cudaMemset2DAsync(P, sizeof(double) * ldp, 0, sizeof(double) * mv, 2 * nb, st));
-  DC_CUDA_TRY(cudaMemset2DAsync(Q, sizeof(double) * ldq, 0, sizeof(double) * nv, 2 * nb, st));
+  // The kernels and the trailing GEMM only read P / Q entries written earlier in
+  // the same panel (rows >= the column's pivot); the zero fill is for callers
+  // that read whole P / Q (labrd_panel returns them as the reference does).
+  if (zero_pq || !g_labrd_skip_zero) {
+    DC_CUDA_TRY(cudaMemset2DAsync(P, sizeof(double) * ldp, 0, sizeof(double) * mv, 2 * nb, st));
+    DC_CUDA_TRY(cudaMemset2DAsync(Q, sizeof(double) * ldq, 0, sizeof(double) * nv, 2 * nb, st));
+  }
   DC_CUDA_TRY(cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned), st));
   LabrdArgs la;
   la.A = Av; la.lda = lda; la.m = mv; la.n = nv; la.nb = nb;
@@ -1496,7 +1502,8 @@ int gebrd_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A
     const int mv = (int)(m - off), nv = (int)(n - off);
     double* Av = A + off + off * lda;
     const int nbp = labrd_panel_width(mv, nv, nb, G);  // same reflectors for any width
-    rc = labrd_launch(h, st, mv, nv, Av, lda, nbp, d + off, e + off, tauq + off, taup + off, P, mp, Q, np, w);
+    rc = labrd_launch(h, st, mv, nv, Av, lda, nbp, d + off, e + off, tauq + off, taup + off, P, mp, Q, np, w,
+                      /*zero_pq=*/false);
     if (rc) return rc;
     // trailing update A[nb:, nb:] -= P[nb:, :] Q[nb:, :]^T  (bidiag.py:195-197)
     GemmDesc gd;
