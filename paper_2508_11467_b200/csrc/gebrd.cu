@@ -1502,8 +1502,10 @@ int gebrd_run(dcsvd_ctx* h, cudaStream_t st, long long m, long long n, double* A
     const int mv = (int)(m - off), nv = (int)(n - off);
     double* Av = A + off + off * lda;
     const int nbp = labrd_panel_width(mv, nv, nb, G);  // same reflectors for any width
+    // whole-GPU handles skip the P / Q zero fill; batch sub-contexts keep it
+    // (measured: C5 12.13 -> 12.50 ms/SVD without it, tools/c5_lib_ab.py)
     rc = labrd_launch(h, st, mv, nv, Av, lda, nbp, d + off, e + off, tauq + off, taup + off, P, mp, Q, np, w,
-                      /*zero_pq=*/false);
+                      /*zero_pq=*/h->is_sub);
     if (rc) return rc;
     // trailing update A[nb:, nb:] -= P[nb:, :] Q[nb:, :]^T  (bidiag.py:195-197)
     GemmDesc gd;
